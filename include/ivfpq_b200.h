@@ -1,0 +1,106 @@
+/*
+ * ivfpq_b200 -- C ABI of the B200-native IVFPQ search path.
+ *
+ * Drop-in boundary for the reference package `ivfpq8`
+ * (/root/reference/pkg/src/ivfpq8).  The reference is pure Python; every
+ * entry point below names the Python function it replaces (file:line), and
+ * INTEGRATION.md shows the ctypes stub a maintainer adds to bind it.
+ *
+ * Conventions
+ *   - plain pointers and sizes only; no torch / CUDA types in signatures
+ *     (`stream` is a cudaStream_t passed as void*, NULL = the handle's stream)
+ *   - every function returns IVFPQ_OK (0) or an error code; the message is in
+ *     ivfpq_last_error() (thread-local).  The Python shim validates arguments
+ *     first and raises ValueError with the reference's wording.
+ *   - "host" entry points take host buffers and are synchronous; "_device"
+ *     entry points take device pointers and are asynchronous on `stream`.
+ *   - LUT dtypes: the reference's `LUT_PRECISIONS` (search.py:38).
+ *   - Keys: uint64 (fp32 bits of the distance << 32 | id), ascending = the
+ *     reference's lexicographic (distance, id) order (search.py:150); empty
+ *     slot = UINT64_MAX.
+ */
+#ifndef IVFPQ_B200_H
+#define IVFPQ_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum ivfpq_lut_dtype { IVFPQ_LUT_F32 = 0, IVFPQ_LUT_F16 = 1, IVFPQ_LUT_E5M3 = 2, IVFPQ_LUT_E4M4 = 3 };
+enum ivfpq_status { IVFPQ_OK = 0, IVFPQ_EINVAL = 1, IVFPQ_ECUDA = 2, IVFPQ_EUNSUPPORTED = 3 };
+
+typedef struct ivfpq_index ivfpq_index; /* opaque device-resident index */
+
+const char *ivfpq_last_error(void);
+int ivfpq_version(void);
+/* Number of visible CUDA devices (0 when no GPU). */
+int ivfpq_device_count(int *n);
+/* Upper bound on k and nprobe supported by the device top-k. */
+int ivfpq_max_k(void);
+
+/* Upload an index.  Replaces the host-resident `IvfPqIndex`
+ * (index.py:27-70): coarse f32[nlist,d] (index.py:35), codebook centers
+ * f32[s, 2^p, d/s] (pq.py:22-23), and the inverted lists in CSR form:
+ * list c = ids[list_off[c] .. list_off[c+1]) with codes row-major
+ * uint8[L_c, s] (index.py:37-38).  `owned` (may be NULL = all lists) selects
+ * the lists this device holds in a list-sharded multi-GPU search; lengths of
+ * all lists are kept for the candidate count.  Ids must be < 2^32-1. */
+int ivfpq_index_create(int device, const float *coarse, int64_t nlist, int64_t d, const float *centers,
+                       int64_t s, int64_t p, const int64_t *list_off, const int64_t *ids,
+                       const uint8_t *codes, const int32_t *owned, int64_t n_owned, ivfpq_index **out);
+int ivfpq_index_destroy(ivfpq_index *idx);
+/* Device bytes held by the index (codes, ids, centroids, codebook). */
+int ivfpq_index_bytes(const ivfpq_index *idx, int64_t *bytes);
+
+/* Replaces search_batch (search.py:187-203): queries f32[nq,d] host;
+ * out_ids int64[nq,k] (-1 padded), out_dists f32[nq,k] (+inf padded),
+ * *out_n_short = rows with fewer than k candidates (search.py:194-202). */
+int ivfpq_search(ivfpq_index *idx, const float *queries, int64_t nq, int64_t k, int64_t nprobe, int lut_dtype,
+                 int64_t *out_ids, float *out_dists, int64_t *out_n_short);
+
+/* Same as ivfpq_search on device buffers; out_short int32[nq] (1 = short). */
+int ivfpq_search_device(ivfpq_index *idx, const float *d_queries, int64_t nq, int64_t k, int64_t nprobe,
+                        int lut_dtype, int64_t *d_out_ids, float *d_out_dists, int32_t *d_out_short,
+                        void *stream);
+
+/* --- staged pieces of the list-sharded multi-GPU search ------------------ */
+/* K1 over the lists this device owns: per query the nprobe smallest
+ * (d2, global cluster id) keys, ascending (select_clusters, search.py:91-97). */
+int ivfpq_select_device(ivfpq_index *idx, const float *d_queries, int64_t nq, int64_t nprobe, uint64_t *d_keys,
+                        void *stream);
+/* Merge W key blocks [W][nq][n_in] (each row ascending) -> [nq][n_out]. */
+int ivfpq_merge_keys_device(const uint64_t *d_in, int64_t W, int64_t nq, int64_t n_in, int64_t n_out,
+                            uint64_t *d_out, void *stream);
+/* K2-K4 over the owned lists among each query's probes (keys from
+ * select/merge): local top-k keys [nq][k] and the global candidate count. */
+int ivfpq_scan_device(ivfpq_index *idx, const float *d_queries, int64_t nq, const uint64_t *d_probe_keys,
+                      int64_t nprobe, int64_t k, int lut_dtype, uint64_t *d_out_keys, int64_t *d_out_ncand,
+                      void *stream);
+/* keys + candidate counts -> ids / dists / short flags (search.py:194-202). */
+int ivfpq_finalize_device(const uint64_t *d_keys, const int64_t *d_ncand, int64_t nq, int64_t k,
+                          int64_t *d_out_ids, float *d_out_dists, int32_t *d_out_short, void *stream);
+
+/* --- conformance hooks (host buffers, run on device 0) -------------------- */
+/* minifloat.py:91-116 encode_array / :119-133 decode_array (dtype e5m3|e4m4) */
+int ivfpq_fp8_encode(const float *x, int64_t n, int lut_dtype, uint8_t *out);
+int ivfpq_fp8_decode(const uint8_t *codes, int64_t n, int lut_dtype, float *out);
+/* minifloat.py:151-164 encode_f16_array / :167-169 decode_f16_array */
+int ivfpq_f16_encode(const float *x, int64_t n, uint16_t *out);
+int ivfpq_f16_decode(const uint16_t *bits, int64_t n, float *out);
+/* search.py:114-127 build_lut: entries [s][2^p] as f32 / u16 / u8 */
+int ivfpq_build_lut(const float *centers, int64_t s, int64_t p, int64_t sub_d, const float *rq, int lut_dtype,
+                    void *out_entries);
+/* search.py:130-142 scan_list: codes row-major uint8[L, s] */
+int ivfpq_scan_list(const uint8_t *codes, int64_t L, int64_t s, int64_t p, const void *entries, int lut_dtype,
+                    float *out_r);
+/* search.py:91-97 select_clusters for host queries q f32[nq,d] -> int64[nq,nprobe] */
+int ivfpq_select_clusters(ivfpq_index *idx, const float *q, int64_t nq, int64_t nprobe, int64_t *out);
+/* search.py:145-155 top_k: out arrays hold min(n, k) entries */
+int ivfpq_top_k(const int64_t *ids, const float *dists, int64_t n, int64_t k, int64_t *out_ids, float *out_dists);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IVFPQ_B200_H */

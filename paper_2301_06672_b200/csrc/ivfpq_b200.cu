@@ -1,0 +1,839 @@
+// ivfpq_b200 -- device index, kernel launches and the C ABI (include/ivfpq_b200.h).
+//
+// Everything here runs on the GPU; there is no CPU compute path.  Host code
+// only validates arguments, moves buffers and launches kernels.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/ivfpq_b200.h"
+#include "codec.cuh"
+#include "coarse.cuh"
+#include "scan.cuh"
+#include "topk.cuh"
+
+using namespace ivfpq;
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CK(call)                                                                                   \
+    do {                                                                                           \
+        cudaError_t e_ = (call);                                                                   \
+        if (e_ != cudaSuccess)                                                                     \
+            return set_err(IVFPQ_ECUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_),    \
+                           __FILE__, __LINE__);                                                    \
+    } while (0)
+
+#define CKR(expr)                    \
+    do {                             \
+        int r_ = (expr);             \
+        if (r_ != IVFPQ_OK) return r_; \
+    } while (0)
+
+constexpr int MAX_K = 4096;
+constexpr size_t SMEM_LIMIT = 227 * 1024;
+constexpr size_t COARSE_CHUNK_BYTES = 256ull << 20;
+
+size_t lut_budget_bytes() {
+    static size_t v = [] {
+        const char* e = getenv("IVFPQ_LUT_BUDGET_KB");
+        return (size_t)(e ? atoi(e) : 64) * 1024;
+    }();
+    return v;
+}
+
+// Device buffer that only grows.
+struct DevBuf {
+    void* p = nullptr;
+    size_t n = 0;
+    int ensure(size_t bytes) {
+        if (bytes <= n) return IVFPQ_OK;
+        if (p) {
+            CK(cudaDeviceSynchronize());
+            CK(cudaFree(p));
+            p = nullptr;
+            n = 0;
+        }
+        CK(cudaMalloc(&p, bytes));
+        n = bytes;
+        return IVFPQ_OK;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    template <class T> T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+}  // namespace
+
+struct ivfpq_index {
+    int device = 0;
+    int64_t nlist = 0, nlist_local = 0, d = 0, s = 0, p = 0, sub_d = 0, s_pad = 0, n_local = 0;
+    float* coarse = nullptr;     // [nlist_local, d]
+    int32_t* l2g = nullptr;      // [nlist_local]
+    int32_t* g2l = nullptr;      // [nlist]
+    int64_t* glen = nullptr;     // [nlist]
+    int64_t* off = nullptr;      // [nlist_local + 1]
+    uint32_t* ids = nullptr;     // [n_local]
+    uint8_t* codes = nullptr;    // [n_local * s_pad] interleaved
+    float* centers = nullptr;    // [s, 2^p, sub_d]
+    int64_t bytes = 0;
+    cudaStream_t stream = nullptr;
+    std::mutex mu;
+    // scratch
+    DevBuf q, dist, pkeys, oids, odist, oshort, keys, ncand;
+};
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+// Row-major [L, s] per list -> interleaved 32-vector blocks of 16-byte chunks:
+// vector v of list c (block b = v/32, nb = min(32, L-32b)), chunk q lives at
+//   (off_c + 32b) * s_pad + q * nb * 16 + (v % 32) * 16.
+__global__ void interleave_codes_kernel(const uint8_t* __restrict__ src, const int64_t* __restrict__ off, int s,
+                                        int s_pad, uint8_t* __restrict__ dst) {
+    const int c = blockIdx.x;
+    const int64_t o = off[c], L = off[c + 1] - o;
+    const int nch = s_pad / 16;
+    for (int64_t i = threadIdx.x; i < L * nch; i += blockDim.x) {
+        const int64_t v = i / nch;
+        const int q = (int)(i - v * nch);
+        const int64_t vb = v & ~31LL;
+        const int nb = (int)(L - vb < 32 ? L - vb : 32);
+        uint8_t* out = dst + (o + vb) * s_pad + (int64_t)q * nb * 16 + (v & 31) * 16;
+        const uint8_t* in = src + (o + v) * s;
+#pragma unroll
+        for (int b = 0; b < 16; ++b) {
+            const int j = q * 16 + b;
+            out[b] = j < s ? in[j] : 0;
+        }
+    }
+}
+
+__global__ void merge_keys_kernel(const uint64_t* __restrict__ in, int W, int nq, int n_in, int n_out,
+                                  uint64_t* __restrict__ out) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    BlockTopK tk;
+    tk.bind(smem, n_out);
+    tk.init();
+    const int total = W * n_in;
+    for (int base = 0; base < total; base += TK_BLOCK) {
+        const int i = base + threadIdx.x;
+        uint64_t key = ~0ull;
+        if (i < total) {
+            const int w = i / n_in, j = i - w * n_in;
+            key = in[((size_t)w * nq + blockIdx.x) * n_in + j];
+        }
+        tk.offer(key, key != ~0ull && key < tk.tau());
+        if (base + TK_BLOCK < total) tk.maybe_merge();
+    }
+    tk.merge();
+    for (int i = threadIdx.x; i < n_out; i += TK_BLOCK) out[(size_t)blockIdx.x * n_out + i] = tk.result()[i];
+}
+
+__global__ void finalize_kernel(const uint64_t* __restrict__ keys, const int64_t* __restrict__ ncand, int nq, int K,
+                                int64_t* __restrict__ ids, float* __restrict__ dists, int32_t* __restrict__ shrt) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < (int64_t)nq * K) {
+        const uint64_t key = keys[i];
+        const bool empty = key == ~0ull;
+        ids[i] = empty ? -1LL : (long long)(uint32_t)key;
+        dists[i] = empty ? __int_as_float(0x7f800000) : __uint_as_float((uint32_t)(key >> 32));
+    }
+    if (i < nq) shrt[i] = ncand[i] < K ? 1 : 0;
+}
+
+__global__ void keys_to_gid_kernel(const uint64_t* __restrict__ keys, int64_t n, int64_t* __restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = (long long)(uint32_t)keys[i];
+}
+
+// ---- conformance-hook kernels ------------------------------------------------
+template <int DT>
+__global__ void encode_kernel(const float* __restrict__ x, int64_t n, typename LutTraits<DT>::T* __restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = lut_store<DT>(x[i]);
+}
+
+template <int DT>
+__global__ void decode_kernel(const typename LutTraits<DT>::T* __restrict__ in, int64_t n, float* __restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        if constexpr (DT == LUT_F16) out[i] = __half2float(__ushort_as_half(in[i]));
+        else out[i] = fp8_decode_exact<LutTraits<DT>::m, LutTraits<DT>::bias>(in[i]);
+    }
+}
+
+// build_lut hook: the same device routine the search kernel uses (ng = 1).
+template <int DT, int LOGN>
+__global__ void __launch_bounds__(TK_BLOCK) build_lut_kernel(const float* centers, int s, int sub_d, const float* rq_g,
+                                                             typename LutTraits<DT>::T* out) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int d = s * sub_d;
+    float* rq = reinterpret_cast<float*>(smem);
+    auto* lut = reinterpret_cast<typename LutTraits<DT>::T*>(smem + (((size_t)d * 4 + 15) & ~(size_t)15));
+    for (int t = threadIdx.x; t < d; t += blockDim.x) rq[t] = rq_g[t];
+    __syncthreads();
+    build_luts<DT, LOGN>(lut, s << LOGN, centers, rq, d, sub_d, 1);
+    __syncthreads();
+    for (int e = threadIdx.x; e < (s << LOGN); e += blockDim.x) out[e] = lut[e];
+}
+
+// scan_list hook: LUT staged in smem, one thread per vector, row-major codes
+// -- the same lookup16 / lut_widen / lut_finish arithmetic as the search kernel.
+template <int DT, int LOGN>
+__global__ void __launch_bounds__(TK_BLOCK) scan_list_kernel(const uint8_t* codes, int64_t L, int s, const void* entries,
+                                                             float* out) {
+    using T = typename LutTraits<DT>::T;
+    extern __shared__ __align__(16) uint8_t smem[];
+    T* lut = reinterpret_cast<T*>(smem);
+    const T* g = reinterpret_cast<const T*>(entries);
+    for (int e = threadIdx.x; e < (s << LOGN); e += blockDim.x) lut[e] = g[e];
+    __syncthreads();
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < L; v += (int64_t)gridDim.x * blockDim.x) {
+        const uint8_t* row = codes + v * s;
+        float acc = 0.0f;
+        for (int j0 = 0; j0 < s; j0 += 16) {
+            uint32_t w[4] = {0, 0, 0, 0};
+            for (int b = 0; b < 16 && j0 + b < s; ++b) w[b >> 2] |= (uint32_t)row[j0 + b] << (8 * (b & 3));
+            acc = lookup16<DT, LOGN, false>(acc, make_uint4(w[0], w[1], w[2], w[3]), lut + (j0 << LOGN), s - j0);
+        }
+        out[v] = lut_finish<DT>(acc);
+    }
+}
+
+// top_k hook: arbitrary fp32 distances -> order-preserving uint32.
+__device__ __forceinline__ uint32_t f32_order(float f) {
+    uint32_t b = __float_as_uint(f == 0.0f ? 0.0f : f);  // -0 == +0 as in numpy
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float f32_unorder(uint32_t u) {
+    return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
+}
+__global__ void topk_hook_kernel(const int64_t* ids, const float* dists, int n, int K, int64_t* out_ids,
+                                 float* out_d) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    BlockTopK tk;
+    tk.bind(smem, K);
+    tk.init();
+    for (int base = 0; base < n; base += TK_BLOCK) {
+        const int i = base + threadIdx.x;
+        uint64_t key = ~0ull;
+        if (i < n) key = ((uint64_t)f32_order(dists[i]) << 32) | (uint32_t)ids[i];
+        tk.offer(key, i < n && key < tk.tau());
+        if (base + TK_BLOCK < n) tk.maybe_merge();
+    }
+    tk.merge();
+    for (int i = threadIdx.x; i < K && i < n; i += TK_BLOCK) {
+        const uint64_t key = tk.result()[i];
+        out_ids[i] = (long long)(uint32_t)key;
+        out_d[i] = f32_unorder((uint32_t)(key >> 32));
+    }
+}
+
+// ---- dispatch -------------------------------------------------------------------
+template <int DT, int LOGN>
+int launch_scan_t(const ScanArgs& a, size_t smem, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        CK(cudaFuncSetAttribute(scan_kernel<DT, LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_LIMIT));
+        attr = true;
+    }
+    scan_kernel<DT, LOGN><<<a.nq, TK_BLOCK, smem, st>>>(a);
+    CK(cudaGetLastError());
+    return IVFPQ_OK;
+}
+
+template <int DT>
+int launch_scan_dt(int logn, const ScanArgs& a, size_t smem, cudaStream_t st) {
+    switch (logn) {
+        case 1: return launch_scan_t<DT, 1>(a, smem, st);
+        case 2: return launch_scan_t<DT, 2>(a, smem, st);
+        case 3: return launch_scan_t<DT, 3>(a, smem, st);
+        case 4: return launch_scan_t<DT, 4>(a, smem, st);
+        case 5: return launch_scan_t<DT, 5>(a, smem, st);
+        case 6: return launch_scan_t<DT, 6>(a, smem, st);
+        case 7: return launch_scan_t<DT, 7>(a, smem, st);
+        case 8: return launch_scan_t<DT, 8>(a, smem, st);
+    }
+    return set_err(IVFPQ_EINVAL, "pq_bits %d out of range 1..8", logn);
+}
+
+#define DISPATCH_DT_LOGN(dt, logn, FN, ...)                                           \
+    [&]() -> int {                                                                    \
+        switch (dt) {                                                                 \
+            case LUT_F32: return FN<LUT_F32>(logn, __VA_ARGS__);                     \
+            case LUT_F16: return FN<LUT_F16>(logn, __VA_ARGS__);                     \
+            case LUT_E5M3: return FN<LUT_E5M3>(logn, __VA_ARGS__);                   \
+            case LUT_E4M4: return FN<LUT_E4M4>(logn, __VA_ARGS__);                   \
+        }                                                                             \
+        return set_err(IVFPQ_EINVAL, "unknown LUT dtype %d", dt);                    \
+    }()
+
+int check_dtype(int dt) {
+    if (dt < 0 || dt > 3) return set_err(IVFPQ_EINVAL, "unknown LUT precision code %d", dt);
+    return IVFPQ_OK;
+}
+
+size_t topk_smem(int K) { return BlockTopK::smem_bytes(K); }
+
+int set_smem_attr(const void* fn, size_t bytes) {
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    return IVFPQ_OK;
+}
+
+cudaStream_t pick_stream(ivfpq_index* idx, void* stream) {
+    return stream ? reinterpret_cast<cudaStream_t>(stream) : idx->stream;
+}
+
+// K1 over the owned centroids: keys [nq, P] (ascending d2, then global id).
+int run_select(ivfpq_index* idx, const float* d_q, int64_t nq, int64_t P, uint64_t* d_keys, cudaStream_t st) {
+    const int64_t nc = idx->nlist_local;
+    if (P > MAX_K) return set_err(IVFPQ_EUNSUPPORTED, "nprobe=%lld exceeds the device limit %d", (long long)P, MAX_K);
+    if (nc == 0) {
+        CK(cudaMemsetAsync(d_keys, 0xff, (size_t)nq * P * 8, st));
+        return IVFPQ_OK;
+    }
+    int64_t rows = std::max<int64_t>(1, std::min<int64_t>(nq, (int64_t)(COARSE_CHUNK_BYTES / (nc * 4))));
+    CKR(idx->dist.ensure((size_t)rows * nc * 4));
+    const size_t sm = topk_smem((int)P);
+    static bool attr = false;
+    if (!attr) {
+        CKR(set_smem_attr((const void*)select_probes_kernel, SMEM_LIMIT));
+        attr = true;
+    }
+    for (int64_t r0 = 0; r0 < nq; r0 += rows) {
+        const int64_t nr = std::min(rows, nq - r0);
+        dim3 grid((unsigned)((nc + CL_BC - 1) / CL_BC), (unsigned)((nr + CL_BQ - 1) / CL_BQ));
+        coarse_l2_kernel<<<grid, 256, 0, st>>>(d_q + r0 * idx->d, (int)nr, idx->coarse, (int)nc, (int)idx->d,
+                                                idx->dist.as<float>());
+        CK(cudaGetLastError());
+        select_probes_kernel<<<(unsigned)nr, TK_BLOCK, sm, st>>>(idx->dist.as<float>(), (int)nc, idx->l2g, (int)P,
+                                                                 d_keys + r0 * P);
+        CK(cudaGetLastError());
+    }
+    return IVFPQ_OK;
+}
+
+int run_scan(ivfpq_index* idx, const float* d_q, int64_t nq, const uint64_t* d_pk, int64_t P, int64_t K, int dt,
+             uint64_t* out_keys, int64_t* out_ncand, int64_t* out_ids, float* out_d, int32_t* out_short,
+             cudaStream_t st) {
+    if (K > MAX_K) return set_err(IVFPQ_EUNSUPPORTED, "k=%lld exceeds the device limit %d", (long long)K, MAX_K);
+    CKR(check_dtype(dt));
+    const size_t lut_each = (size_t)(idx->s << idx->p) * lut_bytes_of(dt);
+    const size_t fixed = ScanSmemLayout((int)idx->d, 1, 0, (int)K).total;
+    if (fixed + lut_each > SMEM_LIMIT)
+        return set_err(IVFPQ_EUNSUPPORTED, "LUT of %zu bytes (s=%lld, p=%lld, dtype %d) does not fit shared memory",
+                       lut_each, (long long)idx->s, (long long)idx->p, dt);
+    int G = (int)std::max<size_t>(1, std::min<size_t>(SCAN_MAX_G, lut_budget_bytes() / lut_each));
+    G = (int)std::min<int64_t>(G, std::max<int64_t>(1, P));
+    while (G > 1 && ScanSmemLayout((int)idx->d, G, lut_each, (int)K).total > SMEM_LIMIT) --G;
+    const size_t smem = ScanSmemLayout((int)idx->d, G, lut_each, (int)K).total;
+    ScanArgs a;
+    a.queries = d_q;
+    a.probes = d_pk;
+    a.coarse = idx->coarse;
+    a.g2l = idx->g2l;
+    a.glen = idx->glen;
+    a.off = idx->off;
+    a.ids = idx->ids;
+    a.codes = idx->codes;
+    a.centers = idx->centers;
+    a.nq = (int)nq;
+    a.d = (int)idx->d;
+    a.P = (int)P;
+    a.s = (int)idx->s;
+    a.sub_d = (int)idx->sub_d;
+    a.s_pad = (int)idx->s_pad;
+    a.K = (int)K;
+    a.G = G;
+    a.out_keys = out_keys;
+    a.out_ncand = out_ncand;
+    a.out_ids = out_ids;
+    a.out_dists = out_d;
+    a.out_short = out_short;
+    if (nq == 0) return IVFPQ_OK;
+    return DISPATCH_DT_LOGN(dt, (int)idx->p, launch_scan_dt, a, smem, st);
+}
+
+int validate_search(ivfpq_index* idx, int64_t nq, int64_t k, int64_t nprobe, int dt) {
+    if (!idx) return set_err(IVFPQ_EINVAL, "null index");
+    if (nq < 0) return set_err(IVFPQ_EINVAL, "nq must be >= 0");
+    if (k < 1) return set_err(IVFPQ_EINVAL, "k must be at least 1");
+    if (nprobe < 1 || nprobe > idx->nlist)
+        return set_err(IVFPQ_EINVAL, "nprobe=%lld out of range 1..%lld", (long long)nprobe, (long long)idx->nlist);
+    if (k > MAX_K) return set_err(IVFPQ_EUNSUPPORTED, "k=%lld exceeds the device limit %d", (long long)k, MAX_K);
+    if (nprobe > MAX_K)
+        return set_err(IVFPQ_EUNSUPPORTED, "nprobe=%lld exceeds the device limit %d", (long long)nprobe, MAX_K);
+    return check_dtype(dt);
+}
+
+int search_device_impl(ivfpq_index* idx, const float* d_q, int64_t nq, int64_t k, int64_t nprobe, int dt,
+                       int64_t* d_ids, float* d_d, int32_t* d_short, cudaStream_t st) {
+    CKR(idx->pkeys.ensure((size_t)std::max<int64_t>(nq, 1) * nprobe * 8));
+    CKR(run_select(idx, d_q, nq, nprobe, idx->pkeys.as<uint64_t>(), st));
+    return run_scan(idx, d_q, nq, idx->pkeys.as<uint64_t>(), nprobe, k, dt, nullptr, nullptr, d_ids, d_d, d_short, st);
+}
+
+unsigned blocks_for(int64_t n, int t = 256) { return (unsigned)std::max<int64_t>(1, (n + t - 1) / t); }
+
+}  // namespace
+
+// =============================================================================
+extern "C" {
+
+const char* ivfpq_last_error(void) { return g_err.c_str(); }
+int ivfpq_version(void) { return 1; }
+int ivfpq_max_k(void) { return MAX_K; }
+
+int ivfpq_device_count(int* n) {
+    int c = 0;
+    cudaError_t e = cudaGetDeviceCount(&c);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        c = 0;
+    }
+    *n = c;
+    return IVFPQ_OK;
+}
+
+int ivfpq_index_create(int device, const float* coarse, int64_t nlist, int64_t d, const float* centers, int64_t s,
+                       int64_t p, const int64_t* list_off, const int64_t* ids, const uint8_t* codes,
+                       const int32_t* owned, int64_t n_owned, ivfpq_index** out) {
+    if (!out) return set_err(IVFPQ_EINVAL, "null output handle");
+    *out = nullptr;
+    if (nlist < 1 || d < 1 || s < 1 || p < 1 || p > 8 || d % s != 0)
+        return set_err(IVFPQ_EINVAL, "invalid index shape nlist=%lld d=%lld s=%lld p=%lld", (long long)nlist,
+                       (long long)d, (long long)s, (long long)p);
+    if (nlist >= (1LL << 31) - 1) return set_err(IVFPQ_EUNSUPPORTED, "nlist too large");
+    const int64_t N = list_off[nlist];
+    if (list_off[0] != 0) return set_err(IVFPQ_EINVAL, "list_off[0] must be 0");
+    for (int64_t c = 0; c < nlist; ++c)
+        if (list_off[c + 1] < list_off[c]) return set_err(IVFPQ_EINVAL, "list_off must be non-decreasing");
+    std::vector<int32_t> own;
+    if (owned) {
+        own.assign(owned, owned + n_owned);
+        for (int32_t c : own)
+            if (c < 0 || c >= nlist) return set_err(IVFPQ_EINVAL, "owned list %d out of range", c);
+        std::sort(own.begin(), own.end());
+        own.erase(std::unique(own.begin(), own.end()), own.end());
+    } else {
+        own.resize(nlist);
+        for (int64_t c = 0; c < nlist; ++c) own[c] = (int32_t)c;
+    }
+    const int64_t sub_d = d / s, n_codes = 1LL << p, s_pad = (s + 15) & ~15LL;
+    const int64_t nl = (int64_t)own.size();
+
+    // gather the owned lists (host staging)
+    std::vector<int64_t> off(nl + 1, 0);
+    for (int64_t i = 0; i < nl; ++i) off[i + 1] = off[i] + (list_off[own[i] + 1] - list_off[own[i]]);
+    const int64_t n_local = off[nl];
+    std::vector<uint32_t> hid(n_local);
+    std::vector<uint8_t> hcodes((size_t)n_local * s);
+    std::vector<float> hco((size_t)nl * d);
+    std::vector<int32_t> l2g(nl), g2l(nlist, -1);
+    std::vector<int64_t> glen(nlist);
+    for (int64_t c = 0; c < nlist; ++c) glen[c] = list_off[c + 1] - list_off[c];
+    for (int64_t i = 0; i < nl; ++i) {
+        const int64_t c = own[i], lo = list_off[c], L = list_off[c + 1] - lo;
+        l2g[i] = (int32_t)c;
+        g2l[c] = (int32_t)i;
+        memcpy(&hco[(size_t)i * d], coarse + (size_t)c * d, sizeof(float) * d);
+        for (int64_t v = 0; v < L; ++v) {
+            const int64_t id = ids[lo + v];
+            if (id < 0 || id >= 0xffffffffLL) return set_err(IVFPQ_EUNSUPPORTED, "id %lld outside [0, 2^32-1)", (long long)id);
+            hid[off[i] + v] = (uint32_t)id;
+        }
+        const uint8_t* src = codes + (size_t)lo * s;
+        for (int64_t b = 0; b < L * s; ++b)
+            if (src[b] >= n_codes) return set_err(IVFPQ_EINVAL, "code byte out of range for p=%lld", (long long)p);
+        memcpy(&hcodes[(size_t)off[i] * s], src, (size_t)L * s);
+    }
+    (void)N;
+
+    DeviceGuard guard(device);
+    CK(cudaSetDevice(device));
+    ivfpq_index* idx = new ivfpq_index();
+    idx->device = device;
+    idx->nlist = nlist;
+    idx->nlist_local = nl;
+    idx->d = d;
+    idx->s = s;
+    idx->p = p;
+    idx->sub_d = sub_d;
+    idx->s_pad = s_pad;
+    idx->n_local = n_local;
+    auto fail = [&](int rc) {
+        ivfpq_index_destroy(idx);
+        return rc;
+    };
+#define CKI(call)                                                                                       \
+    do {                                                                                                \
+        cudaError_t e_ = (call);                                                                        \
+        if (e_ != cudaSuccess)                                                                          \
+            return fail(set_err(IVFPQ_ECUDA, "%s failed: %s", #call, cudaGetErrorString(e_)));          \
+    } while (0)
+    CKI(cudaStreamCreateWithFlags(&idx->stream, cudaStreamNonBlocking));
+    auto up = [&](void** dst, const void* src, size_t bytes) -> cudaError_t {
+        cudaError_t e = cudaMalloc(dst, std::max<size_t>(bytes, 16));
+        if (e != cudaSuccess) return e;
+        idx->bytes += (int64_t)bytes;
+        return bytes ? cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice) : cudaSuccess;
+    };
+    CKI(up((void**)&idx->coarse, hco.data(), hco.size() * 4));
+    CKI(up((void**)&idx->l2g, l2g.data(), l2g.size() * 4));
+    CKI(up((void**)&idx->g2l, g2l.data(), g2l.size() * 4));
+    CKI(up((void**)&idx->glen, glen.data(), glen.size() * 8));
+    CKI(up((void**)&idx->off, off.data(), off.size() * 8));
+    CKI(up((void**)&idx->ids, hid.data(), hid.size() * 4));
+    CKI(up((void**)&idx->centers, centers, (size_t)s * n_codes * sub_d * 4));
+    uint8_t* rowmajor = nullptr;
+    CKI(up((void**)&rowmajor, hcodes.data(), hcodes.size()));
+    CKI(cudaMalloc((void**)&idx->codes, std::max<size_t>((size_t)n_local * s_pad, 16)));
+    idx->bytes += n_local * s_pad - (int64_t)hcodes.size();
+    if (nl > 0) {
+        interleave_codes_kernel<<<(unsigned)nl, 256, 0, idx->stream>>>(rowmajor, idx->off, (int)s, (int)s_pad,
+                                                                       idx->codes);
+        CKI(cudaGetLastError());
+    }
+    CKI(cudaStreamSynchronize(idx->stream));
+    cudaFree(rowmajor);
+#undef CKI
+    *out = idx;
+    return IVFPQ_OK;
+}
+
+int ivfpq_index_destroy(ivfpq_index* idx) {
+    if (!idx) return IVFPQ_OK;
+    DeviceGuard guard(idx->device);
+    if (idx->stream) cudaStreamSynchronize(idx->stream);
+    void* ptrs[] = {idx->coarse, idx->l2g, idx->g2l, idx->glen, idx->off, idx->ids, idx->codes, idx->centers};
+    for (void* ptr : ptrs)
+        if (ptr) cudaFree(ptr);
+    for (DevBuf* b : {&idx->q, &idx->dist, &idx->pkeys, &idx->oids, &idx->odist, &idx->oshort, &idx->keys, &idx->ncand})
+        b->release();
+    if (idx->stream) cudaStreamDestroy(idx->stream);
+    delete idx;
+    return IVFPQ_OK;
+}
+
+int ivfpq_index_bytes(const ivfpq_index* idx, int64_t* bytes) {
+    if (!idx || !bytes) return set_err(IVFPQ_EINVAL, "null argument");
+    *bytes = idx->bytes;
+    return IVFPQ_OK;
+}
+
+int ivfpq_search(ivfpq_index* idx, const float* queries, int64_t nq, int64_t k, int64_t nprobe, int dt,
+                 int64_t* out_ids, float* out_dists, int64_t* out_n_short) {
+    CKR(validate_search(idx, nq, k, nprobe, dt));
+    std::lock_guard<std::mutex> lock(idx->mu);
+    DeviceGuard guard(idx->device);
+    cudaStream_t st = idx->stream;
+    const int64_t nq1 = std::max<int64_t>(nq, 1);
+    CKR(idx->q.ensure((size_t)nq1 * idx->d * 4));
+    CKR(idx->oids.ensure((size_t)nq1 * k * 8));
+    CKR(idx->odist.ensure((size_t)nq1 * k * 4));
+    CKR(idx->oshort.ensure((size_t)nq1 * 4));
+    if (nq > 0) {
+        CK(cudaMemcpyAsync(idx->q.p, queries, (size_t)nq * idx->d * 4, cudaMemcpyHostToDevice, st));
+        CKR(search_device_impl(idx, idx->q.as<float>(), nq, k, nprobe, dt, idx->oids.as<int64_t>(),
+                               idx->odist.as<float>(), idx->oshort.as<int32_t>(), st));
+        CK(cudaMemcpyAsync(out_ids, idx->oids.p, (size_t)nq * k * 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(out_dists, idx->odist.p, (size_t)nq * k * 4, cudaMemcpyDeviceToHost, st));
+    }
+    std::vector<int32_t> sh((size_t)nq);
+    if (nq > 0) CK(cudaMemcpyAsync(sh.data(), idx->oshort.p, (size_t)nq * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    int64_t ns = 0;
+    for (int32_t v : sh) ns += v;
+    if (out_n_short) *out_n_short = ns;
+    return IVFPQ_OK;
+}
+
+int ivfpq_search_device(ivfpq_index* idx, const float* d_q, int64_t nq, int64_t k, int64_t nprobe, int dt,
+                        int64_t* d_ids, float* d_d, int32_t* d_short, void* stream) {
+    CKR(validate_search(idx, nq, k, nprobe, dt));
+    std::lock_guard<std::mutex> lock(idx->mu);
+    DeviceGuard guard(idx->device);
+    if (nq == 0) return IVFPQ_OK;
+    return search_device_impl(idx, d_q, nq, k, nprobe, dt, d_ids, d_d, d_short, pick_stream(idx, stream));
+}
+
+int ivfpq_select_device(ivfpq_index* idx, const float* d_q, int64_t nq, int64_t nprobe, uint64_t* d_keys,
+                        void* stream) {
+    if (!idx) return set_err(IVFPQ_EINVAL, "null index");
+    if (nprobe < 1 || nprobe > idx->nlist)
+        return set_err(IVFPQ_EINVAL, "nprobe=%lld out of range 1..%lld", (long long)nprobe, (long long)idx->nlist);
+    std::lock_guard<std::mutex> lock(idx->mu);
+    DeviceGuard guard(idx->device);
+    if (nq == 0) return IVFPQ_OK;
+    return run_select(idx, d_q, nq, nprobe, d_keys, pick_stream(idx, stream));
+}
+
+int ivfpq_merge_keys_device(const uint64_t* d_in, int64_t W, int64_t nq, int64_t n_in, int64_t n_out,
+                            uint64_t* d_out, void* stream) {
+    if (W < 1 || n_in < 1 || n_out < 1 || n_out > MAX_K)
+        return set_err(IVFPQ_EINVAL, "invalid merge shape W=%lld n_in=%lld n_out=%lld", (long long)W,
+                       (long long)n_in, (long long)n_out);
+    if (nq == 0) return IVFPQ_OK;
+    static bool attr = false;
+    if (!attr) {
+        CKR(set_smem_attr((const void*)merge_keys_kernel, SMEM_LIMIT));
+        attr = true;
+    }
+    merge_keys_kernel<<<(unsigned)nq, TK_BLOCK, topk_smem((int)n_out), reinterpret_cast<cudaStream_t>(stream)>>>(
+        d_in, (int)W, (int)nq, (int)n_in, (int)n_out, d_out);
+    CK(cudaGetLastError());
+    return IVFPQ_OK;
+}
+
+int ivfpq_scan_device(ivfpq_index* idx, const float* d_q, int64_t nq, const uint64_t* d_pk, int64_t nprobe,
+                      int64_t k, int dt, uint64_t* d_keys, int64_t* d_ncand, void* stream) {
+    CKR(validate_search(idx, nq, k, nprobe, dt));
+    std::lock_guard<std::mutex> lock(idx->mu);
+    DeviceGuard guard(idx->device);
+    return run_scan(idx, d_q, nq, d_pk, nprobe, k, dt, d_keys, d_ncand, nullptr, nullptr, nullptr,
+                    pick_stream(idx, stream));
+}
+
+int ivfpq_finalize_device(const uint64_t* d_keys, const int64_t* d_ncand, int64_t nq, int64_t k, int64_t* d_ids,
+                          float* d_d, int32_t* d_short, void* stream) {
+    if (nq == 0) return IVFPQ_OK;
+    const int64_t n = std::max(nq * k, nq);
+    finalize_kernel<<<blocks_for(n), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(d_keys, d_ncand, (int)nq,
+                                                                                      (int)k, d_ids, d_d, d_short);
+    CK(cudaGetLastError());
+    return IVFPQ_OK;
+}
+
+}  // extern "C"
+
+// ---- conformance hooks ---------------------------------------------------------
+namespace {
+template <class T>
+struct Tmp {
+    T* p = nullptr;
+    ~Tmp() {
+        if (p) cudaFree(p);
+    }
+    cudaError_t alloc(size_t n) { return cudaMalloc((void**)&p, std::max<size_t>(n, 1) * sizeof(T)); }
+};
+}  // namespace
+
+extern "C" {
+
+int ivfpq_fp8_encode(const float* x, int64_t n, int dt, uint8_t* out) {
+    if (dt != LUT_E5M3 && dt != LUT_E4M4) return set_err(IVFPQ_EINVAL, "fp8 dtype must be e5m3 or e4m4");
+    if (n == 0) return IVFPQ_OK;
+    Tmp<float> dx;
+    Tmp<uint8_t> dy;
+    CK(dx.alloc(n));
+    CK(dy.alloc(n));
+    CK(cudaMemcpy(dx.p, x, n * 4, cudaMemcpyHostToDevice));
+    if (dt == LUT_E5M3) encode_kernel<LUT_E5M3><<<blocks_for(n), 256>>>(dx.p, n, dy.p);
+    else encode_kernel<LUT_E4M4><<<blocks_for(n), 256>>>(dx.p, n, dy.p);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(out, dy.p, n, cudaMemcpyDeviceToHost));
+    return IVFPQ_OK;
+}
+
+int ivfpq_fp8_decode(const uint8_t* codes, int64_t n, int dt, float* out) {
+    if (dt != LUT_E5M3 && dt != LUT_E4M4) return set_err(IVFPQ_EINVAL, "fp8 dtype must be e5m3 or e4m4");
+    if (n == 0) return IVFPQ_OK;
+    Tmp<uint8_t> dx;
+    Tmp<float> dy;
+    CK(dx.alloc(n));
+    CK(dy.alloc(n));
+    CK(cudaMemcpy(dx.p, codes, n, cudaMemcpyHostToDevice));
+    if (dt == LUT_E5M3) decode_kernel<LUT_E5M3><<<blocks_for(n), 256>>>(dx.p, n, dy.p);
+    else decode_kernel<LUT_E4M4><<<blocks_for(n), 256>>>(dx.p, n, dy.p);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(out, dy.p, n * 4, cudaMemcpyDeviceToHost));
+    return IVFPQ_OK;
+}
+
+int ivfpq_f16_encode(const float* x, int64_t n, uint16_t* out) {
+    if (n == 0) return IVFPQ_OK;
+    Tmp<float> dx;
+    Tmp<uint16_t> dy;
+    CK(dx.alloc(n));
+    CK(dy.alloc(n));
+    CK(cudaMemcpy(dx.p, x, n * 4, cudaMemcpyHostToDevice));
+    encode_kernel<LUT_F16><<<blocks_for(n), 256>>>(dx.p, n, dy.p);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(out, dy.p, n * 2, cudaMemcpyDeviceToHost));
+    return IVFPQ_OK;
+}
+
+int ivfpq_f16_decode(const uint16_t* bits, int64_t n, float* out) {
+    if (n == 0) return IVFPQ_OK;
+    Tmp<uint16_t> dx;
+    Tmp<float> dy;
+    CK(dx.alloc(n));
+    CK(dy.alloc(n));
+    CK(cudaMemcpy(dx.p, bits, n * 2, cudaMemcpyHostToDevice));
+    decode_kernel<LUT_F16><<<blocks_for(n), 256>>>(dx.p, n, dy.p);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(out, dy.p, n * 4, cudaMemcpyDeviceToHost));
+    return IVFPQ_OK;
+}
+
+}  // extern "C"
+
+namespace {
+template <int DT>
+int build_lut_dt(int logn, const float* dc, int s, int sub_d, const float* drq, void* dout, size_t smem) {
+    using T = typename LutTraits<DT>::T;
+    switch (logn) {
+#define BL(L)                                                                                          \
+    case L:                                                                                            \
+        CKR(set_smem_attr((const void*)build_lut_kernel<DT, L>, SMEM_LIMIT));                           \
+        build_lut_kernel<DT, L><<<1, TK_BLOCK, smem>>>(dc, s, sub_d, drq, reinterpret_cast<T*>(dout)); \
+        break;
+        BL(1) BL(2) BL(3) BL(4) BL(5) BL(6) BL(7) BL(8)
+#undef BL
+        default: return set_err(IVFPQ_EINVAL, "pq_bits out of range");
+    }
+    CK(cudaGetLastError());
+    return IVFPQ_OK;
+}
+template <int DT>
+int scan_list_dt(int logn, const uint8_t* dcodes, int64_t L, int s, const void* dent, float* dout, size_t smem) {
+    const unsigned grid = (unsigned)std::min<int64_t>(1024, std::max<int64_t>(1, (L + TK_BLOCK - 1) / TK_BLOCK));
+    switch (logn) {
+#define SL(LG)                                                                                  \
+    case LG:                                                                                    \
+        CKR(set_smem_attr((const void*)scan_list_kernel<DT, LG>, SMEM_LIMIT));                   \
+        scan_list_kernel<DT, LG><<<grid, TK_BLOCK, smem>>>(dcodes, L, s, dent, dout);           \
+        break;
+        SL(1) SL(2) SL(3) SL(4) SL(5) SL(6) SL(7) SL(8)
+#undef SL
+        default: return set_err(IVFPQ_EINVAL, "pq_bits out of range");
+    }
+    CK(cudaGetLastError());
+    return IVFPQ_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int ivfpq_build_lut(const float* centers, int64_t s, int64_t p, int64_t sub_d, const float* rq, int dt,
+                    void* out_entries) {
+    CKR(check_dtype(dt));
+    if (s < 1 || p < 1 || p > 8 || sub_d < 1) return set_err(IVFPQ_EINVAL, "invalid codebook shape");
+    const int64_t d = s * sub_d, ne = s << p;
+    const size_t eb = lut_bytes_of(dt);
+    const size_t smem = (((size_t)d * 4 + 15) & ~(size_t)15) + ne * eb;
+    if (smem > SMEM_LIMIT) return set_err(IVFPQ_EUNSUPPORTED, "LUT does not fit shared memory");
+    Tmp<float> dc, drq;
+    Tmp<uint8_t> dout;
+    CK(dc.alloc(ne * sub_d));
+    CK(drq.alloc(d));
+    CK(dout.alloc(ne * eb));
+    CK(cudaMemcpy(dc.p, centers, ne * sub_d * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(drq.p, rq, d * 4, cudaMemcpyHostToDevice));
+    CKR(DISPATCH_DT_LOGN(dt, (int)p, build_lut_dt, dc.p, (int)s, (int)sub_d, drq.p, dout.p, smem));
+    CK(cudaMemcpy(out_entries, dout.p, ne * eb, cudaMemcpyDeviceToHost));
+    return IVFPQ_OK;
+}
+
+int ivfpq_scan_list(const uint8_t* codes, int64_t L, int64_t s, int64_t p, const void* entries, int dt, float* out_r) {
+    CKR(check_dtype(dt));
+    if (s < 1 || p < 1 || p > 8 || L < 0) return set_err(IVFPQ_EINVAL, "invalid scan shape");
+    const int64_t ne = s << p;
+    const size_t eb = lut_bytes_of(dt);
+    if ((size_t)ne * eb > SMEM_LIMIT) return set_err(IVFPQ_EUNSUPPORTED, "LUT does not fit shared memory");
+    if (L == 0) return IVFPQ_OK;
+    for (int64_t i = 0; i < L * s; ++i)
+        if (codes[i] >= (1 << p)) return set_err(IVFPQ_EINVAL, "code byte out of range for the table");
+    Tmp<uint8_t> dcodes, dent;
+    Tmp<float> dout;
+    CK(dcodes.alloc(L * s));
+    CK(dent.alloc(ne * eb));
+    CK(dout.alloc(L));
+    CK(cudaMemcpy(dcodes.p, codes, L * s, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dent.p, entries, ne * eb, cudaMemcpyHostToDevice));
+    CKR(DISPATCH_DT_LOGN(dt, (int)p, scan_list_dt, dcodes.p, L, (int)s, (const void*)dent.p, dout.p, ne * eb));
+    CK(cudaMemcpy(out_r, dout.p, L * 4, cudaMemcpyDeviceToHost));
+    return IVFPQ_OK;
+}
+
+int ivfpq_select_clusters(ivfpq_index* idx, const float* q, int64_t nq, int64_t nprobe, int64_t* out) {
+    if (!idx) return set_err(IVFPQ_EINVAL, "null index");
+    if (nprobe < 1 || nprobe > idx->nlist)
+        return set_err(IVFPQ_EINVAL, "nprobe=%lld out of range 1..%lld", (long long)nprobe, (long long)idx->nlist);
+    if (nprobe > MAX_K) return set_err(IVFPQ_EUNSUPPORTED, "nprobe exceeds the device limit %d", MAX_K);
+    std::lock_guard<std::mutex> lock(idx->mu);
+    DeviceGuard guard(idx->device);
+    if (nq == 0) return IVFPQ_OK;
+    cudaStream_t st = idx->stream;
+    CKR(idx->q.ensure((size_t)nq * idx->d * 4));
+    CKR(idx->pkeys.ensure((size_t)nq * nprobe * 8));
+    CKR(idx->oids.ensure((size_t)nq * nprobe * 8));
+    CK(cudaMemcpyAsync(idx->q.p, q, (size_t)nq * idx->d * 4, cudaMemcpyHostToDevice, st));
+    CKR(run_select(idx, idx->q.as<float>(), nq, nprobe, idx->pkeys.as<uint64_t>(), st));
+    keys_to_gid_kernel<<<blocks_for(nq * nprobe), 256, 0, st>>>(idx->pkeys.as<uint64_t>(), nq * nprobe,
+                                                                 idx->oids.as<int64_t>());
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, idx->oids.p, (size_t)nq * nprobe * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return IVFPQ_OK;
+}
+
+int ivfpq_top_k(const int64_t* ids, const float* dists, int64_t n, int64_t k, int64_t* out_ids, float* out_dists) {
+    if (n < 1) return set_err(IVFPQ_EINVAL, "top_k requires at least one candidate");
+    if (k < 1) return set_err(IVFPQ_EINVAL, "k must be at least 1");
+    if (k > MAX_K) return set_err(IVFPQ_EUNSUPPORTED, "k exceeds the device limit %d", MAX_K);
+    if (n >= (1LL << 31)) return set_err(IVFPQ_EUNSUPPORTED, "too many candidates");
+    for (int64_t i = 0; i < n; ++i)
+        if (ids[i] < 0 || ids[i] >= 0xffffffffLL) return set_err(IVFPQ_EUNSUPPORTED, "ids must be in [0, 2^32-1)");
+    Tmp<int64_t> di, doi;
+    Tmp<float> dd, dod;
+    CK(di.alloc(n));
+    CK(dd.alloc(n));
+    CK(doi.alloc(k));
+    CK(dod.alloc(k));
+    CK(cudaMemcpy(di.p, ids, n * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dd.p, dists, n * 4, cudaMemcpyHostToDevice));
+    CKR(set_smem_attr((const void*)topk_hook_kernel, SMEM_LIMIT));
+    topk_hook_kernel<<<1, TK_BLOCK, topk_smem((int)k)>>>(di.p, dd.p, (int)n, (int)k, doi.p, dod.p);
+    CK(cudaGetLastError());
+    const int64_t m = std::min(n, k);
+    CK(cudaMemcpy(out_ids, doi.p, m * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(out_dists, dod.p, m * 4, cudaMemcpyDeviceToHost));
+    return IVFPQ_OK;
+}
+
+}  // extern "C"

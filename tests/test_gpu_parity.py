@@ -1,0 +1,227 @@
+"""GPU parity: the sm_100a path vs the reference's golden outputs and the CPU
+oracle, through the C ABI.  Bit-exact everywhere: codec bytes, LUT entries,
+R, probe sets, ids and distances (tolerance 0 -- the kernels reproduce the
+reference's fp32 operation order)."""
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import CASES, GOLDEN, PRECS, index_from_case, load_case
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import paper_2301_06672_b200 as p
+    from paper_2301_06672_b200 import _lib
+
+    if _lib.device_count() < 1:
+        pytest.fail("no CUDA device visible: GPU tests must run on the B200 box")
+    return p
+
+
+@pytest.fixture(scope="module")
+def codec():
+    z = np.load(os.path.join(GOLDEN, "codec.npz"))
+    return {k: z[k] for k in z.files}
+
+
+# ---------------------------------------------------------------- codec ----
+def test_fp8_codec_bit_exact(pkg, codec):
+    for prec, spec in (("e5m3", pkg.E5M3), ("e4m4", pkg.E4M4)):
+        from paper_2301_06672_b200 import minifloat as mf
+        assert np.array_equal(mf.encode_array(codec["x"], spec), codec[prec])
+        assert np.array_equal(mf.decode_table(spec), codec[f"table_{prec}"])
+
+
+def test_f16_codec_bit_exact(pkg, codec):
+    from paper_2301_06672_b200 import minifloat as mf
+    assert np.array_equal(mf.encode_f16_array(codec["x"]), codec["f16"])
+    bits = np.arange(0, 0x7C00, dtype=np.uint16)
+    assert np.array_equal(mf.decode_f16_array(bits), bits.view(np.float16).astype(np.float32))
+
+
+def test_fp8_codec_exhaustive_sweep(pkg):
+    """Every 2^11-th finite non-negative fp32 pattern (~1M values) vs the closed form."""
+    from paper_2301_06672_b200 import minifloat as mf
+    from oracle import ivfpq_np as onp
+    bits = np.arange(0, 0x7F800000, 2039, dtype=np.uint32)
+    x = bits.view(np.float32)
+    for prec, spec in (("e5m3", pkg.E5M3), ("e4m4", pkg.E4M4)):
+        assert np.array_equal(mf.encode_array(x, spec), onp.fp8_encode(x, prec))
+    assert np.array_equal(mf.encode_f16_array(x), onp.f16_encode(x))
+
+
+def test_codec_known_answers(pkg):
+    from paper_2301_06672_b200 import minifloat as mf
+    E5M3, E4M4 = pkg.E5M3, pkg.E4M4
+    assert mf.encode(0.0, E5M3) == 0x00 and mf.encode(1.0, E5M3) == 0x78
+    assert mf.decode(0x78, E5M3) == 1.0 and mf.decode(0xFF, E5M3) == 122880.0
+    assert mf.decode(mf.encode(1.3, E5M3), E5M3) == 1.25
+    assert mf.encode(2.0 ** 20, E5M3) == 0xFF
+    assert mf.encode(float(np.nextafter(np.float32(122880.0), np.float32(np.inf))), E5M3) == 0xFF
+    assert mf.encode(float(np.nextafter(np.float32(2.0 ** -14), np.float32(0))), E5M3) == 0x00
+    assert mf.encode(1e-30, E4M4) == 0x00
+    for mant in range(8):
+        assert mf.decode(mant, E5M3) == 0.0
+    assert mf.encode_f16(1.0) == 0x3C00 and mf.encode_f16(65504.0) == 0x7BFF
+    assert mf.encode_f16(1e9) == 0x7BFF and mf.encode_f16(65520.0) == 0x7BFF
+    assert mf.encode_f16(1.0 + 2.0 ** -11) == 0x3C00 and mf.encode_f16(1.0 + 3 * 2.0 ** -11) == 0x3C02
+    with pytest.raises(AssertionError):
+        mf.encode(-1.0, E5M3)
+
+
+# ------------------------------------------------------------ K2 / K3 -----
+@pytest.mark.parametrize("name", CASES)
+def test_build_lut_and_scan_bit_exact(pkg, name):
+    c = load_case(name)
+    idx = index_from_case(c)
+    for n, (qi, cl) in enumerate(c["lut_pairs"]):
+        rq = c["queries"][qi] - c["coarse"][cl]
+        for prec in PRECS:
+            lut = pkg.build_lut(idx.cb, rq, prec)
+            assert np.array_equal(lut.entries, c[f"lut_{prec}_{n}"]), (name, n, prec)
+            _, r = pkg.scan_list(idx.list_ids[cl], idx.list_codes[cl], lut)
+            assert np.array_equal(r, c[f"scan_{prec}_{n}"]), (name, n, prec)
+
+
+def test_build_lut_p6_codebook(pkg):
+    z = np.load(os.path.join(GOLDEN, "codebook_p6.npz"))
+    cb = pkg.PQCodebook(centers=z["centers"], p=6)
+    for i in range(z["rq"].shape[0]):
+        for prec in PRECS:
+            lut = pkg.build_lut(cb, z["rq"][i], prec)
+            assert np.array_equal(lut.entries, z[f"lut_{prec}_{i}"])
+    # exact codeword row -> zero entries in every precision (test_search.py:97-101)
+    for prec in PRECS:
+        assert np.all(pkg.build_lut(cb, z["rq"][3], prec).decoded()[:, 5] == 0.0)
+
+
+def test_scan_list_known_answers(pkg):
+    lut = pkg.Lut(entries=np.arange(16, dtype=np.float32).reshape(1, 16), precision="f32")
+    _, r = pkg.scan_list(np.array([0, 1]), np.array([[3], [9]], dtype=np.uint8), lut)
+    assert r.tolist() == [3.0, 9.0]
+    lut = pkg.Lut(entries=np.zeros((4, 16), np.float32), precision="f32")
+    codes = np.random.default_rng(0).integers(0, 16, (5, 4)).astype(np.uint8)
+    assert np.all(pkg.scan_list(np.arange(5), codes, lut)[1] == 0.0)
+
+
+# ------------------------------------------------------------------ K4 ----
+def test_top_k_known_answers(pkg):
+    res = pkg.top_k(np.array([5, 2, 9]), np.float32([0.3, 0.1, 0.2]), k=10)
+    assert res.ids.tolist() == [2, 9, 5] and res.short
+    res = pkg.top_k(np.array([7, 3, 5, 1]), np.zeros(4, np.float32), k=2)
+    assert res.ids.tolist() == [1, 3] and not res.short
+    rng = np.random.default_rng(7)
+    ids = rng.permutation(1000)
+    d = rng.random(1000).astype(np.float32)
+    d[rng.integers(0, 1000, 100)] = 0.5
+    res = pkg.top_k(ids, d, 10)
+    expect = sorted(zip(d.tolist(), ids.tolist()))[:10]
+    assert res.ids.tolist() == [i for _, i in expect]
+    assert res.distances.tolist() == [x for x, _ in expect]
+
+
+# ------------------------------------------------------------------ K1 ----
+@pytest.mark.parametrize("name", CASES)
+def test_select_clusters_bit_exact(pkg, name):
+    c = load_case(name)
+    idx = index_from_case(c)
+    P = c["select"].shape[1]
+    for qi, q in enumerate(c["queries"]):
+        assert np.array_equal(pkg.select_clusters(idx, q, P), c["select"][qi])
+    with pytest.raises(ValueError, match="nprobe"):
+        pkg.select_clusters(idx, c["queries"][0], idx.nlist + 1)
+
+
+# ----------------------------------------------------------- end to end ---
+@pytest.mark.parametrize("name", CASES)
+def test_search_batch_bit_exact_vs_reference(pkg, name):
+    c = load_case(name)
+    idx = index_from_case(c)
+    for k, nprobe in c["runs"]:
+        for prec in PRECS:
+            tag = f"{prec}_k{k}_p{nprobe}"
+            lists, n_short = pkg.search_batch(idx, c["queries"], pkg.SearchParams(k=int(k), nprobe=int(nprobe),
+                                                                                  precision=prec))
+            assert np.array_equal(lists.ids, c[f"ids_{tag}"]), (name, tag)
+            assert np.array_equal(lists.distances, c[f"d_{tag}"]), (name, tag)
+            assert n_short == int(c[f"short_{tag}"]), (name, tag)
+
+
+def test_search_single_query_api(pkg):
+    c = load_case("small")
+    idx = index_from_case(c)
+    res = pkg.search(idx, c["queries"][0], pkg.SearchParams(k=2000, nprobe=16, precision="f32"))
+    assert np.array_equal(res.ids, c["ids_f32_k2000_p16"][0]) and not res.short
+    blobs = index_from_case(load_case("blobs"))
+    lists, n_short = pkg.search_batch(blobs, np.zeros((1, 4), np.float32), pkg.SearchParams(k=20, nprobe=1))
+    assert n_short == 1 and (lists.ids[0] == -1).sum() == 4
+    assert np.all(np.isinf(lists.distances[0][lists.ids[0] == -1]))
+
+
+def _random_index(rng, n, d, s, p, nlist, empty_lists=()):
+    from paper_2301_06672_b200.index import IvfPqIndex, PQCodebook
+    coarse = rng.random((nlist, d)).astype(np.float32)
+    centers = (rng.standard_normal((s, 1 << p, d // s)) * 0.3).astype(np.float32)
+    assign = rng.integers(0, nlist, n)
+    for e in empty_lists:
+        assign[assign == e] = (e + 1) % nlist
+    order = np.argsort(assign, kind="stable")
+    off = np.searchsorted(assign[order], np.arange(nlist + 1)).astype(np.int64)
+    codes = rng.integers(0, 1 << p, (n, s)).astype(np.uint8)[order]
+    return IvfPqIndex.from_csr(coarse, PQCodebook(centers=centers, p=p), off, order.astype(np.int64), codes)
+
+
+@pytest.mark.parametrize("shape", [
+    dict(n=30000, d=128, s=64, p=8, nlist=64, P=8, k=10),        # SIFT-shaped, multi-block lists
+    dict(n=20000, d=96, s=48, p=8, nlist=32, P=5, k=100),        # DEEP cfg4 shape, k=100
+    dict(n=20000, d=96, s=32, p=8, nlist=32, P=6, k=10),         # cfg5 shape (sub_d = 3)
+    dict(n=8000, d=120, s=24, p=5, nlist=16, P=4, k=10),         # p=5, s not a multiple of 16
+    dict(n=5000, d=40, s=20, p=4, nlist=8, P=8, k=64),           # p=4, nprobe = nlist
+])
+def test_search_batch_vs_c_oracle_random(pkg, shape):
+    from oracle import c_oracle
+    rng = np.random.default_rng(shape["n"] + shape["s"])
+    idx = _random_index(rng, shape["n"], shape["d"], shape["s"], shape["p"], shape["nlist"], empty_lists=(3,))
+    q = rng.random((64, shape["d"])).astype(np.float32)
+    off, ids, codes = idx.csr()
+    for prec in PRECS:
+        got, n_short = pkg.search_batch(idx, q, pkg.SearchParams(k=shape["k"], nprobe=shape["P"], precision=prec))
+        want_ids, want_d, want_short = c_oracle.search_batch(idx.coarse, idx.cb.centers, off, ids, codes, q,
+                                                             shape["k"], shape["P"], prec)
+        assert np.array_equal(got.ids, want_ids), prec
+        assert np.array_equal(got.distances, want_d), prec
+        assert n_short == want_short
+
+
+def test_search_device_api_matches_host_api(pkg):
+    import torch
+    c = load_case("sift_mini")
+    idx = index_from_case(c)
+    params = pkg.SearchParams(k=10, nprobe=8, precision="e5m3")
+    host, _ = pkg.search_batch(idx, c["queries"], params)
+    dev = pkg.device_index(idx)
+    q = torch.from_numpy(c["queries"]).cuda()
+    oi = torch.empty((q.shape[0], 10), dtype=torch.int64, device="cuda")
+    od = torch.empty((q.shape[0], 10), dtype=torch.float32, device="cuda")
+    osh = torch.empty(q.shape[0], dtype=torch.int32, device="cuda")
+    pkg.search_device(dev, q, params, oi, od, osh)
+    torch.cuda.synchronize()
+    assert np.array_equal(oi.cpu().numpy(), host.ids)
+    assert np.array_equal(od.cpu().numpy(), host.distances)
+
+
+def test_recall_against_reference_gt(pkg):
+    c = load_case("sift_mini")
+    gt = np.load(os.path.join(GOLDEN, "sift_mini_gt.npz"))
+    idx = index_from_case(c)
+    r = {}
+    for prec in PRECS:
+        lists, _ = pkg.search_batch(idx, c["queries"], pkg.SearchParams(k=10, nprobe=8, precision=prec))
+        r[prec] = pkg.recall(lists, pkg.NeighborLists(ids=gt["ids"]))[1]
+    assert r["f32"] > 0.3
+    assert abs(r["e5m3"] - r["f32"]) <= 0.05 and abs(r["e4m4"] - r["f32"]) <= 0.05
