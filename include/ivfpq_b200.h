@@ -8,7 +8,8 @@
  *
  * Conventions
  *   - plain pointers and sizes only; no torch / CUDA types in signatures
- *     (`stream` is a cudaStream_t passed as void*, NULL = the handle's stream)
+ *     (`stream` is a cudaStream_t passed as void*; NULL = the legacy default
+ *     stream, as in the CUDA runtime)
  *   - every function returns IVFPQ_OK (0) or an error code; the message is in
  *     ivfpq_last_error() (thread-local).  The Python shim validates arguments
  *     first and raises ValueError with the reference's wording.
@@ -39,6 +40,8 @@ int ivfpq_version(void);
 int ivfpq_device_count(int *n);
 /* Upper bound on k and nprobe supported by the device top-k. */
 int ivfpq_max_k(void);
+/* Number of CUDA kernels this library has launched since it was loaded. */
+int ivfpq_launch_count(int64_t *out);
 
 /* Upload an index.  Replaces the host-resident `IvfPqIndex`
  * (index.py:27-70): coarse f32[nlist,d] (index.py:35), codebook centers

@@ -28,6 +28,7 @@ SIGNATURES = {
     "ivfpq_version": [],
     "ivfpq_device_count": [_P],
     "ivfpq_max_k": [],
+    "ivfpq_launch_count": [_P],
     "ivfpq_index_create": [_I32, _P, _I64, _I64, _P, _I64, _I64, _P, _P, _P, _P, _I64, _P],
     "ivfpq_index_destroy": [_P],
     "ivfpq_index_bytes": [_P, _P],
@@ -98,6 +99,12 @@ def require_gpu() -> None:
 
 def max_k() -> int:
     return int(lib.ivfpq_max_k())
+
+
+def launch_count() -> int:
+    n = ctypes.c_int64(0)
+    check(lib.ivfpq_launch_count(ctypes.byref(n)))
+    return n.value
 
 
 def ptr(a) -> int:

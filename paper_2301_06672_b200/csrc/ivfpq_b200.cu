@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -40,6 +41,15 @@ int set_err(int code, const char* fmt, ...) {
         if (e_ != cudaSuccess)                                                                     \
             return set_err(IVFPQ_ECUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_),    \
                            __FILE__, __LINE__);                                                    \
+    } while (0)
+
+std::atomic<long long> g_launches{0};
+
+// After every kernel launch: count it (ivfpq_launch_count) and check it.
+#define KCHECK()                                              \
+    do {                                                      \
+        g_launches.fetch_add(1, std::memory_order_relaxed);   \
+        CK(cudaGetLastError());                               \
     } while (0)
 
 #define CKR(expr)                    \
@@ -272,7 +282,7 @@ int launch_scan_t(const ScanArgs& a, size_t smem, cudaStream_t st) {
         attr = true;
     }
     scan_kernel<DT, LOGN><<<a.nq, TK_BLOCK, smem, st>>>(a);
-    CK(cudaGetLastError());
+    KCHECK();
     return IVFPQ_OK;
 }
 
@@ -314,9 +324,9 @@ int set_smem_attr(const void* fn, size_t bytes) {
     return IVFPQ_OK;
 }
 
-cudaStream_t pick_stream(ivfpq_index* idx, void* stream) {
-    return stream ? reinterpret_cast<cudaStream_t>(stream) : idx->stream;
-}
+// `stream` is used as given: NULL is the legacy default stream, exactly as in
+// the CUDA runtime (torch's default stream has handle 0).
+cudaStream_t pick_stream(ivfpq_index*, void* stream) { return reinterpret_cast<cudaStream_t>(stream); }
 
 // K1 over the owned centroids: keys [nq, P] (ascending d2, then global id).
 int run_select(ivfpq_index* idx, const float* d_q, int64_t nq, int64_t P, uint64_t* d_keys, cudaStream_t st) {
@@ -339,10 +349,10 @@ int run_select(ivfpq_index* idx, const float* d_q, int64_t nq, int64_t P, uint64
         dim3 grid((unsigned)((nc + CL_BC - 1) / CL_BC), (unsigned)((nr + CL_BQ - 1) / CL_BQ));
         coarse_l2_kernel<<<grid, 256, 0, st>>>(d_q + r0 * idx->d, (int)nr, idx->coarse, (int)nc, (int)idx->d,
                                                 idx->dist.as<float>());
-        CK(cudaGetLastError());
+        KCHECK();
         select_probes_kernel<<<(unsigned)nr, TK_BLOCK, sm, st>>>(idx->dist.as<float>(), (int)nc, idx->l2g, (int)P,
                                                                  d_keys + r0 * P);
-        CK(cudaGetLastError());
+        KCHECK();
     }
     return IVFPQ_OK;
 }
@@ -417,6 +427,12 @@ extern "C" {
 const char* ivfpq_last_error(void) { return g_err.c_str(); }
 int ivfpq_version(void) { return 1; }
 int ivfpq_max_k(void) { return MAX_K; }
+
+int ivfpq_launch_count(int64_t* out) {
+    if (!out) return set_err(IVFPQ_EINVAL, "null argument");
+    *out = g_launches.load();
+    return IVFPQ_OK;
+}
 
 int ivfpq_device_count(int* n) {
     int c = 0;
@@ -526,6 +542,7 @@ int ivfpq_index_create(int device, const float* coarse, int64_t nlist, int64_t d
     if (nl > 0) {
         interleave_codes_kernel<<<(unsigned)nl, 256, 0, idx->stream>>>(rowmajor, idx->off, (int)s, (int)s_pad,
                                                                        idx->codes);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
         CKI(cudaGetLastError());
     }
     CKI(cudaStreamSynchronize(idx->stream));
@@ -615,7 +632,7 @@ int ivfpq_merge_keys_device(const uint64_t* d_in, int64_t W, int64_t nq, int64_t
     }
     merge_keys_kernel<<<(unsigned)nq, TK_BLOCK, topk_smem((int)n_out), reinterpret_cast<cudaStream_t>(stream)>>>(
         d_in, (int)W, (int)nq, (int)n_in, (int)n_out, d_out);
-    CK(cudaGetLastError());
+    KCHECK();
     return IVFPQ_OK;
 }
 
@@ -634,7 +651,7 @@ int ivfpq_finalize_device(const uint64_t* d_keys, const int64_t* d_ncand, int64_
     const int64_t n = std::max(nq * k, nq);
     finalize_kernel<<<blocks_for(n), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(d_keys, d_ncand, (int)nq,
                                                                                       (int)k, d_ids, d_d, d_short);
-    CK(cudaGetLastError());
+    KCHECK();
     return IVFPQ_OK;
 }
 
@@ -664,7 +681,7 @@ int ivfpq_fp8_encode(const float* x, int64_t n, int dt, uint8_t* out) {
     CK(cudaMemcpy(dx.p, x, n * 4, cudaMemcpyHostToDevice));
     if (dt == LUT_E5M3) encode_kernel<LUT_E5M3><<<blocks_for(n), 256>>>(dx.p, n, dy.p);
     else encode_kernel<LUT_E4M4><<<blocks_for(n), 256>>>(dx.p, n, dy.p);
-    CK(cudaGetLastError());
+    KCHECK();
     CK(cudaMemcpy(out, dy.p, n, cudaMemcpyDeviceToHost));
     return IVFPQ_OK;
 }
@@ -679,7 +696,7 @@ int ivfpq_fp8_decode(const uint8_t* codes, int64_t n, int dt, float* out) {
     CK(cudaMemcpy(dx.p, codes, n, cudaMemcpyHostToDevice));
     if (dt == LUT_E5M3) decode_kernel<LUT_E5M3><<<blocks_for(n), 256>>>(dx.p, n, dy.p);
     else decode_kernel<LUT_E4M4><<<blocks_for(n), 256>>>(dx.p, n, dy.p);
-    CK(cudaGetLastError());
+    KCHECK();
     CK(cudaMemcpy(out, dy.p, n * 4, cudaMemcpyDeviceToHost));
     return IVFPQ_OK;
 }
@@ -692,7 +709,7 @@ int ivfpq_f16_encode(const float* x, int64_t n, uint16_t* out) {
     CK(dy.alloc(n));
     CK(cudaMemcpy(dx.p, x, n * 4, cudaMemcpyHostToDevice));
     encode_kernel<LUT_F16><<<blocks_for(n), 256>>>(dx.p, n, dy.p);
-    CK(cudaGetLastError());
+    KCHECK();
     CK(cudaMemcpy(out, dy.p, n * 2, cudaMemcpyDeviceToHost));
     return IVFPQ_OK;
 }
@@ -705,7 +722,7 @@ int ivfpq_f16_decode(const uint16_t* bits, int64_t n, float* out) {
     CK(dy.alloc(n));
     CK(cudaMemcpy(dx.p, bits, n * 2, cudaMemcpyHostToDevice));
     decode_kernel<LUT_F16><<<blocks_for(n), 256>>>(dx.p, n, dy.p);
-    CK(cudaGetLastError());
+    KCHECK();
     CK(cudaMemcpy(out, dy.p, n * 4, cudaMemcpyDeviceToHost));
     return IVFPQ_OK;
 }
@@ -726,7 +743,7 @@ int build_lut_dt(int logn, const float* dc, int s, int sub_d, const float* drq, 
 #undef BL
         default: return set_err(IVFPQ_EINVAL, "pq_bits out of range");
     }
-    CK(cudaGetLastError());
+    KCHECK();
     return IVFPQ_OK;
 }
 template <int DT>
@@ -742,7 +759,7 @@ int scan_list_dt(int logn, const uint8_t* dcodes, int64_t L, int s, const void* 
 #undef SL
         default: return set_err(IVFPQ_EINVAL, "pq_bits out of range");
     }
-    CK(cudaGetLastError());
+    KCHECK();
     return IVFPQ_OK;
 }
 }  // namespace
@@ -806,7 +823,7 @@ int ivfpq_select_clusters(ivfpq_index* idx, const float* q, int64_t nq, int64_t 
     CKR(run_select(idx, idx->q.as<float>(), nq, nprobe, idx->pkeys.as<uint64_t>(), st));
     keys_to_gid_kernel<<<blocks_for(nq * nprobe), 256, 0, st>>>(idx->pkeys.as<uint64_t>(), nq * nprobe,
                                                                  idx->oids.as<int64_t>());
-    CK(cudaGetLastError());
+    KCHECK();
     CK(cudaMemcpyAsync(out, idx->oids.p, (size_t)nq * nprobe * 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     return IVFPQ_OK;
@@ -829,7 +846,7 @@ int ivfpq_top_k(const int64_t* ids, const float* dists, int64_t n, int64_t k, in
     CK(cudaMemcpy(dd.p, dists, n * 4, cudaMemcpyHostToDevice));
     CKR(set_smem_attr((const void*)topk_hook_kernel, SMEM_LIMIT));
     topk_hook_kernel<<<1, TK_BLOCK, topk_smem((int)k)>>>(di.p, dd.p, (int)n, (int)k, doi.p, dod.p);
-    CK(cudaGetLastError());
+    KCHECK();
     const int64_t m = std::min(n, k);
     CK(cudaMemcpy(out_ids, doi.p, m * 8, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(out_dists, dod.p, m * 4, cudaMemcpyDeviceToHost));

@@ -225,3 +225,64 @@ def test_recall_against_reference_gt(pkg):
         r[prec] = pkg.recall(lists, pkg.NeighborLists(ids=gt["ids"]))[1]
     assert r["f32"] > 0.3
     assert abs(r["e5m3"] - r["f32"]) <= 0.05 and abs(r["e4m4"] - r["f32"]) <= 0.05
+
+
+def test_sharded_protocol_emulated_on_one_gpu(pkg):
+    """The multi-GPU protocol with 3 list shards held as 3 handles on one GPU
+    (run one after another; 'all-gather' = stack): bit-identical to 1 GPU."""
+    import torch
+    from paper_2301_06672_b200 import parallel
+    from paper_2301_06672_b200.index import DeviceIndex
+    c = load_case("sift_mini")
+    idx = index_from_case(c)
+    shards = parallel.shard_lists(np.diff(c["list_off"]), idx.cb.s, 3)
+    ops = [parallel.CudaShardOps(DeviceIndex(idx, 0, owned=sh)) for sh in shards]
+    q = torch.from_numpy(c["queries"]).cuda()
+    for prec in PRECS:
+        for k, P in ((10, 8), (100, 4)):
+            ids, d, short = parallel.sharded_search(_StackOps(ops), q, k, P, prec, lambda t: t)
+            assert np.array_equal(ids.cpu().numpy(), c[f"ids_{prec}_k{k}_p{P}"]), (prec, k, P)
+            assert np.array_equal(d.cpu().numpy(), c[f"d_{prec}_k{k}_p{P}"]), (prec, k, P)
+            assert int(short.sum()) == int(c[f"short_{prec}_k{k}_p{P}"])
+
+
+class _StackOps:
+    """Adapter: runs every shard's op and returns the stacked result, so that
+    `all_gather` is the identity on the already-stacked tensors."""
+
+    def __init__(self, ops):
+        self.ops = ops
+
+    def select(self, q, P):
+        import torch
+        return torch.stack([o.select(q, P) for o in self.ops])
+
+    def merge(self, stacked, n):
+        return self.ops[0].merge(stacked, n)
+
+    def scan(self, q, probes, P, k, prec):
+        import torch
+        outs = [o.scan(q, probes, P, k, prec) for o in self.ops]
+        for o in outs[1:]:
+            assert torch.equal(o[1], outs[0][1])
+        return torch.stack([o[0] for o in outs]), outs[0][1]
+
+    def finalize(self, keys, ncand, k):
+        return self.ops[0].finalize(keys, ncand, k)
+
+
+def test_device_search_on_side_stream(pkg):
+    import torch
+    c = load_case("sift_mini")
+    idx = index_from_case(c)
+    params = pkg.SearchParams(k=10, nprobe=8, precision="f16")
+    dev = pkg.device_index(idx)
+    q = torch.from_numpy(c["queries"]).cuda()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        oi = torch.full((q.shape[0], 10), 7, dtype=torch.int64, device="cuda")
+        od = torch.empty((q.shape[0], 10), dtype=torch.float32, device="cuda")
+        osh = torch.empty(q.shape[0], dtype=torch.int32, device="cuda")
+        pkg.search_device(dev, q, params, oi, od, osh)
+        got = oi.cpu().numpy()
+    assert np.array_equal(got, c["ids_f16_k10_p8"])
