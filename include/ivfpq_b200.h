@@ -40,6 +40,10 @@ int ivfpq_version(void);
 int ivfpq_device_count(int *n);
 /* Upper bound on k and nprobe supported by the device top-k. */
 int ivfpq_max_k(void);
+/* Scan kernel selection (testing): 0 = auto (persistent warp-specialised
+ * kernel when the shape fits, else the per-query kernel), 1 = force the
+ * per-query kernel. */
+int ivfpq_set_scan_kernel(int mode);
 /* Number of CUDA kernels this library has launched since it was loaded. */
 int ivfpq_launch_count(int64_t *out);
 

@@ -18,6 +18,7 @@
 #include "coarse.cuh"
 #include "scan.cuh"
 #include "topk.cuh"
+#include "ws_launch.cuh"
 
 using namespace ivfpq;
 
@@ -111,7 +112,8 @@ struct ivfpq_index {
     cudaStream_t stream = nullptr;
     std::mutex mu;
     // scratch
-    DevBuf q, dist, pkeys, oids, odist, oshort, keys, ncand;
+    DevBuf q, dist, pkeys, oids, odist, oshort, keys, ncand, work;
+    int num_sms = 0;
 };
 
 namespace {
@@ -357,6 +359,48 @@ int run_select(ivfpq_index* idx, const float* d_q, int64_t nq, int64_t P, uint64
     return IVFPQ_OK;
 }
 
+struct WsPlan {
+    int G, NBUF;
+    size_t smem;
+};
+
+// 0 = auto (v2 when the shape fits), 1 = force v1; set by ivfpq_set_scan_kernel
+// or the IVFPQ_SCAN_V1 environment variable.
+std::atomic<int> g_scan_mode{-1};
+
+bool ws_disabled() {
+    int m = g_scan_mode.load();
+    if (m < 0) {
+        const char* e = getenv("IVFPQ_SCAN_V1");
+        m = (e && atoi(e) != 0) ? 1 : 0;
+        g_scan_mode.store(m);
+    }
+    return m == 1;
+}
+
+// Can the v2 kernel run this shape?  Builder registers: ceil(s / R) subspaces
+// of a 4-code quad, R = 1024 / 2^p row groups, at most 32 / sub_d of them.
+bool ws_plan(const ivfpq_index* idx, int64_t P, int64_t K, int dt, WsPlan* plan) {
+    if (ws_disabled() || idx->num_sms <= 0) return false;
+    const int64_t N = 1LL << idx->p;
+    if (idx->p < 2 || idx->sub_d < 1 || idx->sub_d > 4 || K > WS_MAX_K) return false;
+    const int64_t R = 1024 / N;
+    const int64_t jpt = 32 / idx->sub_d;
+    if ((idx->s + R - 1) / R > jpt) return false;
+    const size_t lut_each = (size_t)idx->s * N * lut_bytes_of((int)dt);
+    int G = (int)std::max<size_t>(1, std::min<size_t>(WS_MAX_G, lut_budget_bytes() / lut_each));
+    G = (int)std::min<int64_t>(G, std::max<int64_t>(1, P));
+    for (; G >= 1; --G)
+        for (int nb = WS_MAX_NBUF; nb >= 2; --nb) {
+            const size_t sm = WsLayout((int)idx->d, G, nb, lut_each, (int)K).total;
+            if (sm <= SMEM_LIMIT) {
+                *plan = WsPlan{G, nb, sm};
+                return true;
+            }
+        }
+    return false;
+}
+
 int run_scan(ivfpq_index* idx, const float* d_q, int64_t nq, const uint64_t* d_pk, int64_t P, int64_t K, int dt,
              uint64_t* out_keys, int64_t* out_ncand, int64_t* out_ids, float* out_d, int32_t* out_short,
              cudaStream_t st) {
@@ -395,6 +439,29 @@ int run_scan(ivfpq_index* idx, const float* d_q, int64_t nq, const uint64_t* d_p
     a.out_dists = out_d;
     a.out_short = out_short;
     if (nq == 0) return IVFPQ_OK;
+    // v2 (persistent, warp-specialised, register-resident codebook) when the
+    // shape fits its register/smem budget; v1 otherwise.
+    WsPlan plan;
+    if (ws_plan(idx, P, K, dt, &plan)) {
+        a.G = plan.G;
+        WsArgs w;
+        w.a = a;
+        w.NBUF = plan.NBUF;
+        CKR(idx->work.ensure(16));
+        w.work = idx->work.as<int>();
+        CK(cudaMemsetAsync(w.work, 0, sizeof(int), st));
+        const int grid = std::min<int64_t>(idx->num_sms, nq);
+        cudaError_t e = cudaErrorInvalidValue;
+        switch (dt) {
+            case LUT_F32: e = ws_launch_f32((int)idx->p, (int)idx->sub_d, w, plan.smem, grid, st); break;
+            case LUT_F16: e = ws_launch_f16((int)idx->p, (int)idx->sub_d, w, plan.smem, grid, st); break;
+            case LUT_E5M3: e = ws_launch_e5m3((int)idx->p, (int)idx->sub_d, w, plan.smem, grid, st); break;
+            case LUT_E4M4: e = ws_launch_e4m4((int)idx->p, (int)idx->sub_d, w, plan.smem, grid, st); break;
+        }
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        if (e != cudaSuccess) return set_err(IVFPQ_ECUDA, "scan_ws launch failed: %s", cudaGetErrorString(e));
+        return IVFPQ_OK;
+    }
     return DISPATCH_DT_LOGN(dt, (int)idx->p, launch_scan_dt, a, smem, st);
 }
 
@@ -427,6 +494,12 @@ extern "C" {
 const char* ivfpq_last_error(void) { return g_err.c_str(); }
 int ivfpq_version(void) { return 1; }
 int ivfpq_max_k(void) { return MAX_K; }
+
+int ivfpq_set_scan_kernel(int mode) {
+    if (mode < 0 || mode > 1) return set_err(IVFPQ_EINVAL, "scan kernel mode must be 0 (auto) or 1 (v1)");
+    g_scan_mode.store(mode);
+    return IVFPQ_OK;
+}
 
 int ivfpq_launch_count(int64_t* out) {
     if (!out) return set_err(IVFPQ_EINVAL, "null argument");
@@ -522,6 +595,7 @@ int ivfpq_index_create(int device, const float* coarse, int64_t nlist, int64_t d
             return fail(set_err(IVFPQ_ECUDA, "%s failed: %s", #call, cudaGetErrorString(e_)));          \
     } while (0)
     CKI(cudaStreamCreateWithFlags(&idx->stream, cudaStreamNonBlocking));
+    CKI(cudaDeviceGetAttribute(&idx->num_sms, cudaDevAttrMultiProcessorCount, device));
     auto up = [&](void** dst, const void* src, size_t bytes) -> cudaError_t {
         cudaError_t e = cudaMalloc(dst, std::max<size_t>(bytes, 16));
         if (e != cudaSuccess) return e;
@@ -559,7 +633,8 @@ int ivfpq_index_destroy(ivfpq_index* idx) {
     void* ptrs[] = {idx->coarse, idx->l2g, idx->g2l, idx->glen, idx->off, idx->ids, idx->codes, idx->centers};
     for (void* ptr : ptrs)
         if (ptr) cudaFree(ptr);
-    for (DevBuf* b : {&idx->q, &idx->dist, &idx->pkeys, &idx->oids, &idx->odist, &idx->oshort, &idx->keys, &idx->ncand})
+    for (DevBuf* b : {&idx->q, &idx->dist, &idx->pkeys, &idx->oids, &idx->odist, &idx->oshort, &idx->keys, &idx->ncand,
+                      &idx->work})
         b->release();
     if (idx->stream) cudaStreamDestroy(idx->stream);
     delete idx;

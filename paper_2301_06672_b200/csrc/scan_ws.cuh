@@ -1,0 +1,484 @@
+// K2 + K3 + K4, v2: persistent, warp-specialised search kernel for sm_100a.
+//
+// Same arithmetic as the reference (search.py:158-184 -> build_lut :114-127,
+// scan_list :130-142, top_k :145-155) and as scan.cuh, restructured for B200:
+//
+//  * one CTA per SM (persistent), queries handed out by a global atomic;
+//  * 8 BUILDER warps (2 warpgroups, setmaxnreg 168) keep the whole PQ codebook
+//    in registers: builder thread t owns a quad of codes m = 4u..4u+3 and the
+//    subspaces j = jr, jr+R, ... (u = t % (N/4), jr = t / (N/4), R = 1024/N).
+//    Per (j, quad) one broadcast read of rq[j] feeds 4 table entries computed
+//    with packed f32x2 sub/mul/add (exact: every op is one IEEE rounding, in
+//    the reference order), then stored with one 4-, 8- or 16-byte STS:
+//      fp8: mul.rz.ftz.f32x2 by 2^-(127-bias) (exact scaling; values below
+//           min_normal become subnormal and flush to +0), then the code is
+//           min(bits >> (23-m), 255), done two-at-a-time with u16x2 min.
+//      f16: cvt.rn.satfinite.f16x2.f32 (= RNE of min(x, 65504)).
+//  * 12 SCANNER warps (3 warpgroups, setmaxnreg 56) stream 32-vector code
+//    blocks (16-byte non-allocating loads, interleaved layout) and look the
+//    codes up in the slot's LUTs; R accumulates sequentially in j (fp32).
+//  * builders and scanners exchange LUT slots (NBUF of them, each holding the
+//    LUTs of G probed lists of one query) through mbarriers: full[] (256
+//    builder arrivals) and empty[] (one arrival per scanner warp), so building
+//    job i+1 overlaps scanning job i and scanner warps never wait on each other.
+//  * top-k: each scanner warp filters against the query's shared threshold and
+//    appends survivors to a private smem buffer; a full buffer is rank-sorted
+//    and merged into the query's shared sorted list under a per-query lock.
+//    The last warp to finish a query writes its results.
+#pragma once
+#include <stdint.h>
+
+#include "codec.cuh"
+#include "scan.cuh"
+
+namespace ivfpq {
+
+constexpr int WS_BW = 8;                     // builder warps
+constexpr int WS_SW = 12;                    // scanner warps
+constexpr int WS_NB = WS_BW * 32;            // 256 builder threads
+constexpr int WS_THREADS = (WS_BW + WS_SW) * 32;
+constexpr int WS_MAX_G = 8;
+constexpr int WS_MAX_NBUF = 3;
+constexpr int WS_WBUF = 64;                  // per-warp candidate buffer
+constexpr int WS_MAX_K = 512;
+constexpr int WS_BAR_BUILD = 1;              // named barrier id for builders
+
+struct WsArgs {
+    ScanArgs a;            // inputs/outputs shared with the v1 kernel
+    int NBUF;
+    int* work;             // global query counter (zeroed before launch)
+};
+
+struct WsJob {
+    int qs, q, ng, last, nblk, pad;
+    int pref[WS_MAX_G + 1];
+    int len[WS_MAX_G];
+    int lc[WS_MAX_G];
+    long long off[WS_MAX_G];
+};
+
+struct WsQuery {
+    uint64_t tau;
+    long long ncand;
+    int lock, done, cur, q;
+};
+
+// ---------------------------------------------------------------- PTX helpers
+typedef uint64_t u64;
+__device__ __forceinline__ u64 pk2(float a, float b) {
+    u64 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void upk2(u64 v, float& a, float& b) { asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v)); }
+__device__ __forceinline__ u64 sub2(u64 a, u64 b) {
+    u64 r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ u64 mul2(u64 a, u64 b) {
+    u64 r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+// Two scalar add.rn.f32 on the halves.  NOT add.rn.f32x2: ptxas (12.9)
+// contracts mul.rn.f32x2 -> add.rn.f32x2 into FFMA2 even with --fmad=false,
+// which would change the reference's rounding; scalar .rn adds are kept.
+__device__ __forceinline__ u64 add2(u64 a, u64 b) {
+    u64 r;
+    asm("{\n\t.reg .f32 a0, a1, b0, b1;\n\t"
+        "mov.b64 {a0, a1}, %1;\n\tmov.b64 {b0, b1}, %2;\n\t"
+        "add.rn.f32 a0, a0, b0;\n\tadd.rn.f32 a1, a1, b1;\n\t"
+        "mov.b64 %0, {a0, a1};\n\t}"
+        : "=l"(r)
+        : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ u64 mulrzftz2(u64 a, u64 b) {
+    u64 r;
+    asm("mul.rz.ftz.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ uint32_t min_u16x2(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("min.u16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+__device__ __forceinline__ uint32_t cvt_f16x2_sat(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+
+__device__ __forceinline__ void mbar_init(u64* bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(u64* bar) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(u64* bar, uint32_t parity) {
+    const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bar_builders() { asm volatile("bar.sync %0, %1;" ::"n"(WS_BAR_BUILD), "n"(WS_NB) : "memory"); }
+
+// --------------------------------------------------------------- smem layout
+struct WsLayout {
+    size_t bars, jobs, qst, lists, wbuf, rq, lut, total;
+    __host__ __device__ WsLayout(int d, int G, int NBUF, size_t lut_each, int K) {
+        bars = 0;                                                        // full[NBUF], empty[NBUF]
+        jobs = 64;                                                       // WsJob[NBUF]
+        qst = jobs + WS_MAX_NBUF * sizeof(WsJob);                        // WsQuery[NBUF+1]
+        qst = (qst + 15) & ~(size_t)15;
+        lists = qst + (WS_MAX_NBUF + 1) * sizeof(WsQuery);               // u64[NBUF+1][2][K]
+        lists = (lists + 15) & ~(size_t)15;
+        wbuf = lists + (size_t)(NBUF + 1) * 2 * K * 8;                   // u64[SW][2][WBUF]
+        rq = wbuf + (size_t)WS_SW * 2 * WS_WBUF * 8;                     // f32[NBUF][G][d]
+        lut = rq + (((size_t)NBUF * G * d * 4 + 15) & ~(size_t)15);      // [NBUF][G][lut_each]
+        total = lut + (size_t)NBUF * G * ((lut_each + 15) & ~(size_t)15);
+    }
+};
+
+// ------------------------------------------------------------- the builders
+// JPT: compile-time bound on the subspaces one builder thread owns.
+template <int DT, int LOGN, int SUB_D>
+struct WsBuild {
+    static constexpr int N = 1 << LOGN;
+    static constexpr int NQ4 = N / 4;               // quads per subspace row
+    static constexpr int R = WS_NB / NQ4;           // row groups
+    static constexpr int JPT = 32 / SUB_D;          // 4 * JPT * SUB_D <= 128 registers
+    using T = typename LutTraits<DT>::T;
+
+    u64 cen[JPT][2][SUB_D];  // (c[m0], c[m0+1]) and (c[m0+2], c[m0+3]) per owned j, per dim
+    int u, jr;
+
+    __device__ void load(const float* __restrict__ centers, int s, int t) {
+        u = t % NQ4;
+        jr = t / NQ4;
+#pragma unroll
+        for (int i = 0; i < JPT; ++i) {
+            const int j = jr + R * i;
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int x = 0; x < SUB_D; ++x) {
+                    float a = 0.f, b = 0.f;
+                    if (j < s) {
+                        const size_t e = (size_t)j * N + 4 * u + 2 * h;
+                        a = __ldg(centers + e * SUB_D + x);
+                        b = __ldg(centers + (e + 1) * SUB_D + x);
+                    }
+                    cen[i][h][x] = pk2(a, b);
+                }
+        }
+    }
+
+    // One table (one probed list): rq[d] in smem -> lut (s x N entries) in smem.
+    __device__ __forceinline__ void build(const float* rq, T* lut, int s) const {
+#pragma unroll
+        for (int i = 0; i < JPT; ++i) {
+            const int j = jr + R * i;
+            if (j < s) {
+                u64 acc0 = 0, acc1 = 0;
+#pragma unroll
+                for (int x = 0; x < SUB_D; ++x) {
+                    const float r = rq[j * SUB_D + x];
+                    const u64 rr = pk2(r, r);
+                    const u64 d0 = sub2(cen[i][0][x], rr), d1 = sub2(cen[i][1][x], rr);
+                    const u64 q0 = mul2(d0, d0), q1 = mul2(d1, d1);
+                    // acc starts at +0: fl(0 + q) = q exactly (q >= +0)
+                    acc0 = x == 0 ? q0 : add2(acc0, q0);
+                    acc1 = x == 0 ? q1 : add2(acc1, q1);
+                }
+                store(lut + (size_t)j * N + 4 * u, acc0, acc1);
+            }
+        }
+    }
+
+    __device__ __forceinline__ static void store(T* dst, u64 a01, u64 a23) {
+        if constexpr (DT == LUT_F32) {
+            float a0, a1, a2, a3;
+            upk2(a01, a0, a1);
+            upk2(a23, a2, a3);
+            *reinterpret_cast<float4*>(dst) = make_float4(a0, a1, a2, a3);
+        } else if constexpr (DT == LUT_F16) {
+            float a0, a1, a2, a3;
+            upk2(a01, a0, a1);
+            upk2(a23, a2, a3);
+            *reinterpret_cast<uint2*>(dst) = make_uint2(cvt_f16x2_sat(a0, a1), cvt_f16x2_sat(a2, a3));
+        } else {
+            constexpr int M = LutTraits<DT>::m, BIAS = LutTraits<DT>::bias;
+            // y = x * 2^-(127-bias), round-toward-zero + flush-to-zero: exact
+            // for x >= min_normal, +0 below it (never rounds up into range).
+            const float sc = __uint_as_float((uint32_t)(127 - (127 - BIAS)) << 23);
+            const u64 s2 = pk2(sc, sc);
+            const u64 y01 = mulrzftz2(a01, s2), y23 = mulrzftz2(a23, s2);
+            float f0, f1, f2, f3;
+            upk2(y01, f0, f1);
+            upk2(y23, f2, f3);
+            // code = min(bits >> (23-M), 255) = min(bits >> 16, lim) >> (7-M), two per u16x2
+            constexpr uint32_t lim = (256u << (7 - M)) - 1u;  // 0x0FFF (m=3) / 0x07FF (m=4)
+            uint32_t h01 = __byte_perm(__float_as_uint(f0), __float_as_uint(f1), 0x7632);
+            uint32_t h23 = __byte_perm(__float_as_uint(f2), __float_as_uint(f3), 0x7632);
+            h01 = min_u16x2(h01, lim | (lim << 16)) >> (7 - M);
+            h23 = min_u16x2(h23, lim | (lim << 16)) >> (7 - M);
+            *reinterpret_cast<uint32_t*>(dst) = __byte_perm(h01, h23, 0x6420);
+        }
+    }
+};
+
+// ------------------------------------------------------------- warp top-k
+struct WarpTopK {
+    u64* buf;      // WS_WBUF
+    u64* srt;      // WS_WBUF
+    int n;         // warp-uniform count
+
+    __device__ __forceinline__ void offer(u64 key, bool pred) {
+        const unsigned m = __ballot_sync(0xffffffffu, pred);
+        if (pred) buf[n + __popc(m & ((1u << (threadIdx.x & 31)) - 1))] = key;
+        n += __popc(m);
+    }
+
+    // Merge the buffer into the query's shared list (lock held by this warp).
+    __device__ void flush(WsQuery* S, u64* lists, int K) {
+        const int lane = threadIdx.x & 31;
+        __syncwarp();
+        for (int i = lane; i < n; i += 32) {
+            const u64 x = buf[i];
+            int r = 0;
+            for (int j = 0; j < n; ++j) r += buf[j] < x;
+            srt[r] = x;
+        }
+        if (lane == 0) {
+            while (atomicCAS(&S->lock, 0, 1) != 0) {
+            }
+            __threadfence_block();
+        }
+        __syncwarp();
+        const int cur = *(volatile int*)&S->cur;
+        const u64* A = lists + (size_t)cur * K;
+        u64* O = lists + (size_t)(cur ^ 1) * K;
+        for (int i = lane; i < K; i += 32) {
+            const u64 a = A[i];
+            const int pos = i + lower_bound_u64(srt, n, a);
+            if (pos < K) O[pos] = a;
+        }
+        for (int i = lane; i < n; i += 32) {
+            const u64 b = srt[i];
+            const int pos = i + lower_bound_u64(A, K, b);
+            if (pos < K) O[pos] = b;
+        }
+        __syncwarp();
+        if (lane == 0) {
+            *(volatile int*)&S->cur = cur ^ 1;
+            *(volatile u64*)&S->tau = O[K - 1];
+            __threadfence_block();
+            atomicExch(&S->lock, 0);
+        }
+        __syncwarp();
+        n = 0;
+    }
+};
+
+template <int DT, int LOGN, int SUB_D>
+__global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) {
+    using T = typename LutTraits<DT>::T;
+    constexpr int N = 1 << LOGN;
+    extern __shared__ __align__(16) uint8_t smem[];
+    const ScanArgs& a = w.a;
+    const int G = a.G, NBUF = w.NBUF, K = a.K, NQS = NBUF + 1;
+    const int lut_elems = a.s << LOGN;
+    const size_t lut_each = ((size_t)lut_elems * sizeof(T) + 15) & ~(size_t)15;
+    const WsLayout L(a.d, G, NBUF, (size_t)lut_elems * sizeof(T), K);
+    u64* full = reinterpret_cast<u64*>(smem + L.bars);
+    u64* empty = full + WS_MAX_NBUF;
+    WsJob* jobs = reinterpret_cast<WsJob*>(smem + L.jobs);
+    WsQuery* qst = reinterpret_cast<WsQuery*>(smem + L.qst);
+    u64* lists = reinterpret_cast<u64*>(smem + L.lists);
+    float* rq_all = reinterpret_cast<float*>(smem + L.rq);
+    uint8_t* lut_all = smem + L.lut;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    // ---- setup
+    for (int i = threadIdx.x; i < NQS * 2 * K; i += blockDim.x) lists[i] = ~0ull;
+    if (threadIdx.x < NQS) {
+        WsQuery* S = qst + threadIdx.x;
+        S->tau = ~0ull;
+        S->ncand = 0;
+        S->lock = 0;
+        S->done = 0;
+        S->cur = 0;
+        S->q = -1;
+    }
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < NBUF; ++b) {
+            mbar_init(full + b, WS_NB);
+            mbar_init(empty + b, WS_SW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp < WS_BW) {
+        // =========================== builders ===========================
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 168;\n");
+        const int t = threadIdx.x;
+        WsBuild<DT, LOGN, SUB_D> B;
+        B.load(a.centers, a.s, t);
+        int q = -1, cursor = a.P, qseq = -1;  // q/cursor/qseq meaningful in thread 0
+        for (int job = 0;; ++job) {
+            const int slot = job % NBUF;
+            if (job >= NBUF) mbar_wait(empty + slot, ((job / NBUF) - 1) & 1);
+            WsJob* J = jobs + slot;
+            if (t == 0) {
+                // next job: up to G valid probes of the current query, or a new query
+                if (cursor >= a.P) {
+                    q = atomicAdd(w.work, 1);
+                    cursor = 0;
+                    ++qseq;
+                    if (q < a.nq) {
+                        WsQuery* S = qst + (qseq % NQS);
+                        S->q = q;
+                        S->ncand = 0;
+                    }
+                }
+                if (q >= a.nq) {
+                    J->qs = -1;
+                } else {
+                    WsQuery* S = qst + (qseq % NQS);
+                    const u64* probes = a.probes + (size_t)q * a.P;
+                    int ng = 0, pref = 0;
+                    long long nc = 0;
+                    while (cursor < a.P) {
+                        const u64 key = probes[cursor];
+                        const uint32_t gid = (uint32_t)key;
+                        const int lc = key == ~0ull ? -1 : a.g2l[gid];
+                        const long long o = lc >= 0 ? a.off[lc] : 0;
+                        const long long len = lc >= 0 ? a.off[lc + 1] - o : 0;
+                        if (len > 0 && ng == G) break;   // next job starts here
+                        ++cursor;
+                        if (key != ~0ull) nc += a.glen[gid];
+                        if (len == 0) continue;
+                        J->lc[ng] = lc;
+                        J->len[ng] = (int)len;
+                        J->off[ng] = o;
+                        J->pref[ng] = pref;
+                        pref += (int)((len + 31) >> 5);
+                        ++ng;
+                    }
+                    S->ncand += nc;
+                    J->qs = qseq % NQS;
+                    J->q = q;
+                    J->ng = ng;
+                    J->pref[ng] = pref;
+                    J->nblk = pref;
+                    J->last = cursor >= a.P;
+                }
+            }
+            bar_builders();
+            const int qs = J->qs;
+            if (qs < 0) {
+                mbar_arrive(full + slot);
+                break;
+            }
+            const int ng = J->ng, jq = J->q;
+            float* rq = rq_all + (size_t)slot * G * a.d;
+            for (int i = t; i < ng * a.d; i += WS_NB) {
+                const int g = i / a.d, x = i - g * a.d;
+                rq[i] = __fsub_rn(__ldg(a.queries + (size_t)jq * a.d + x), __ldg(a.coarse + (size_t)J->lc[g] * a.d + x));
+            }
+            bar_builders();
+            T* lut = reinterpret_cast<T*>(lut_all + (size_t)slot * G * lut_each);
+            for (int g = 0; g < ng; ++g)
+                B.build(rq + (size_t)g * a.d, reinterpret_cast<T*>(reinterpret_cast<uint8_t*>(lut) + g * lut_each), a.s);
+            mbar_arrive(full + slot);
+        }
+    } else {
+        // =========================== scanners ===========================
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n");
+        const int sw = warp - WS_BW;
+        u64* wb = reinterpret_cast<u64*>(smem + L.wbuf) + (size_t)sw * 2 * WS_WBUF;
+        WarpTopK tk{wb, wb + WS_WBUF, 0};
+        for (int job = 0;; ++job) {
+            const int slot = job % NBUF;
+            mbar_wait(full + slot, (job / NBUF) & 1);
+            const WsJob* J = jobs + slot;
+            const int qs = J->qs;
+            if (qs < 0) break;
+            WsQuery* S = qst + qs;
+            u64* qlist = lists + (size_t)qs * 2 * K;
+            const int ng = J->ng, nblk = J->nblk;
+            const uint8_t* lutb = lut_all + (size_t)slot * G * lut_each;
+            for (int b = sw; b < nblk; b += WS_SW) {
+                int g = 0;
+                while (g + 1 < ng && b >= J->pref[g + 1]) ++g;
+                const int vstart = (b - J->pref[g]) * 32;
+                const int len = J->len[g];
+                const int nb = min(32, len - vstart);
+                const long long vo = J->off[g] + vstart;
+                u64 key = ~0ull;
+                bool pass = false;
+                if (lane < nb) {
+                    const uint8_t* vb = a.codes + (size_t)vo * a.s_pad + lane * 16;
+                    const float R = scan_vector<DT, LOGN>(vb, nb, reinterpret_cast<const T*>(lutb + g * lut_each), a.s);
+                    const uint32_t rb = __float_as_uint(R);
+                    const u64 tau = *(volatile u64*)&S->tau;
+                    if (rb <= (uint32_t)(tau >> 32)) {
+                        key = ((u64)rb << 32) | a.ids[vo + lane];
+                        pass = key < tau;
+                    }
+                }
+                tk.offer(key, pass);
+                if (tk.n > WS_WBUF - 32) tk.flush(S, qlist, K);
+            }
+            if (tk.n > 0) tk.flush(S, qlist, K);
+            if (J->last) {
+                int d = 0;
+                if (lane == 0) d = atomicAdd(&S->done, 1);
+                d = __shfl_sync(0xffffffffu, d, 0);
+                if (d == WS_SW - 1) {
+                    // last warp for this query: results + reset of the query state
+                    __threadfence_block();
+                    const int cur = *(volatile int*)&S->cur;
+                    const u64* r = qlist + (size_t)cur * K;
+                    const int q = S->q;
+                    const long long nc = S->ncand;
+                    for (int i = lane; i < K; i += 32) {
+                        const u64 key = r[i];
+                        if (a.out_keys) {
+                            a.out_keys[(size_t)q * K + i] = key;
+                        } else {
+                            const bool e = key == ~0ull;
+                            a.out_ids[(size_t)q * K + i] = e ? -1LL : (long long)(uint32_t)key;
+                            a.out_dists[(size_t)q * K + i] = e ? __int_as_float(0x7f800000) : __uint_as_float((uint32_t)(key >> 32));
+                        }
+                    }
+                    if (lane == 0) {
+                        if (a.out_keys) a.out_ncand[q] = nc;
+                        else a.out_short[q] = nc < K ? 1 : 0;
+                    }
+                    __syncwarp();
+                    for (int i = lane; i < 2 * K; i += 32) qlist[i] = ~0ull;
+                    if (lane == 0) {
+                        S->tau = ~0ull;
+                        S->cur = 0;
+                        S->done = 0;
+                    }
+                    __threadfence_block();
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty + slot);
+        }
+    }
+}
+
+}  // namespace ivfpq

@@ -124,3 +124,13 @@ def test_product_package_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 text = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.sub(r"#.*|//.*", "", text).replace("oracle/", ""), f
+
+
+def test_no_fma_contraction_in_device_code():
+    """Bit-exactness needs every fp32 op rounded on its own (the reference runs
+    one numpy ufunc per op): no FFMA/FFMA2 may appear in the shipped SASS."""
+    import subprocess
+    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", _lib.LIB_PATH], capture_output=True,
+                          text=True).stdout
+    assert "FADD" in sass and "LDS" in sass
+    assert "FFMA" not in sass

@@ -23,6 +23,16 @@ def pkg():
     return p
 
 
+@pytest.fixture(params=["auto", "v1"])
+def scan_kernel(request, pkg):
+    """Run a test with the persistent warp-specialised scan (auto) and with the
+    per-query scan kernel (v1)."""
+    from paper_2301_06672_b200 import _lib
+    _lib.check(_lib.lib.ivfpq_set_scan_kernel(0 if request.param == "auto" else 1))
+    yield request.param
+    _lib.check(_lib.lib.ivfpq_set_scan_kernel(0))
+
+
 @pytest.fixture(scope="module")
 def codec():
     z = np.load(os.path.join(GOLDEN, "codec.npz"))
@@ -139,7 +149,7 @@ def test_select_clusters_bit_exact(pkg, name):
 
 # ----------------------------------------------------------- end to end ---
 @pytest.mark.parametrize("name", CASES)
-def test_search_batch_bit_exact_vs_reference(pkg, name):
+def test_search_batch_bit_exact_vs_reference(pkg, name, scan_kernel):
     c = load_case(name)
     idx = index_from_case(c)
     for k, nprobe in c["runs"]:
@@ -183,7 +193,7 @@ def _random_index(rng, n, d, s, p, nlist, empty_lists=()):
     dict(n=8000, d=120, s=24, p=5, nlist=16, P=4, k=10),         # p=5, s not a multiple of 16
     dict(n=5000, d=40, s=20, p=4, nlist=8, P=8, k=64),           # p=4, nprobe = nlist
 ])
-def test_search_batch_vs_c_oracle_random(pkg, shape):
+def test_search_batch_vs_c_oracle_random(pkg, shape, scan_kernel):
     from oracle import c_oracle
     rng = np.random.default_rng(shape["n"] + shape["s"])
     idx = _random_index(rng, shape["n"], shape["d"], shape["s"], shape["p"], shape["nlist"], empty_lists=(3,))
@@ -227,7 +237,7 @@ def test_recall_against_reference_gt(pkg):
     assert abs(r["e5m3"] - r["f32"]) <= 0.05 and abs(r["e4m4"] - r["f32"]) <= 0.05
 
 
-def test_sharded_protocol_emulated_on_one_gpu(pkg):
+def test_sharded_protocol_emulated_on_one_gpu(pkg, scan_kernel):
     """The multi-GPU protocol with 3 list shards held as 3 handles on one GPU
     (run one after another; 'all-gather' = stack): bit-identical to 1 GPU."""
     import torch
