@@ -458,9 +458,13 @@ int run_scan(ivfpq_index* idx, const float* d_q, int64_t nq, const uint64_t* d_p
             case LUT_E5M3: e = ws_launch_e5m3((int)idx->p, (int)idx->sub_d, w, plan.smem, grid, st); break;
             case LUT_E4M4: e = ws_launch_e4m4((int)idx->p, (int)idx->sub_d, w, plan.smem, grid, st); break;
         }
-        g_launches.fetch_add(1, std::memory_order_relaxed);
-        if (e != cudaSuccess) return set_err(IVFPQ_ECUDA, "scan_ws launch failed: %s", cudaGetErrorString(e));
-        return IVFPQ_OK;
+        if (e == cudaSuccess) {
+            g_launches.fetch_add(1, std::memory_order_relaxed);
+            return IVFPQ_OK;
+        }
+        if (e != cudaErrorNotSupported)
+            return set_err(IVFPQ_ECUDA, "scan_ws launch failed: %s", cudaGetErrorString(e));
+        a.G = G;  // register budget not met by this build: per-query kernel
     }
     return DISPATCH_DT_LOGN(dt, (int)idx->p, launch_scan_dt, a, smem, st);
 }

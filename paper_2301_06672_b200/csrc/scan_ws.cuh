@@ -14,7 +14,7 @@
 //           min_normal become subnormal and flush to +0), then the code is
 //           min(bits >> (23-m), 255), done two-at-a-time with u16x2 min.
 //      f16: cvt.rn.satfinite.f16x2.f32 (= RNE of min(x, 65504)).
-//  * 12 SCANNER warps (3 warpgroups, setmaxnreg 56) stream 32-vector code
+//  * 12 SCANNER warps (3 warpgroups, setmaxnreg 48) stream 32-vector code
 //    blocks (16-byte non-allocating loads, interleaved layout) and look the
 //    codes up in the slot's LUTs; R accumulates sequentially in j (fp32).
 //  * builders and scanners exchange LUT slots (NBUF of them, each holding the
@@ -42,6 +42,13 @@ constexpr int WS_MAX_NBUF = 3;
 constexpr int WS_WBUF = 64;                  // per-warp candidate buffer
 constexpr int WS_MAX_K = 512;
 constexpr int WS_BAR_BUILD = 1;              // named barrier id for builders
+// setmaxnreg budget: .inc draws only on registers released by .dec inside the
+// CTA, so WS_NB*WS_REG_B + WS_NS*WS_REG_S must not exceed the launch
+// allocation WS_THREADS * regs (ptxas gives 96 at 640 threads; the host
+// checks cudaFuncAttributes::numRegs before using this kernel).
+constexpr int WS_REG_B = 168;
+constexpr int WS_REG_S = 48;
+constexpr int WS_NS = WS_SW * 32;
 
 struct WsArgs {
     ScanArgs a;            // inputs/outputs shared with the v1 kernel
@@ -329,7 +336,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
 
     if (warp < WS_BW) {
         // =========================== builders ===========================
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 168;\n");
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(WS_REG_B));
         const int t = threadIdx.x;
         WsBuild<DT, LOGN, SUB_D> B;
         B.load(a.centers, a.s, t);
@@ -403,7 +410,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
         }
     } else {
         // =========================== scanners ===========================
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n");
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(WS_REG_S));
         const int sw = warp - WS_BW;
         u64* wb = reinterpret_cast<u64*>(smem + L.wbuf) + (size_t)sw * 2 * WS_WBUF;
         WarpTopK tk{wb, wb + WS_WBUF, 0};

@@ -9,13 +9,18 @@ namespace ivfpq {
 
 template <int DT, int LOGN, int SUB_D>
 cudaError_t ws_launch_t(const WsArgs& w, size_t smem, int grid, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
+    static int ok = -1;
+    if (ok < 0) {
         cudaError_t e = cudaFuncSetAttribute(scan_ws_kernel<DT, LOGN, SUB_D>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         if (e != cudaSuccess) return e;
-        attr = true;
+        cudaFuncAttributes fa;
+        e = cudaFuncGetAttributes(&fa, scan_ws_kernel<DT, LOGN, SUB_D>);
+        if (e != cudaSuccess) return e;
+        // setmaxnreg.inc must be satisfiable from the registers .dec releases
+        ok = fa.numRegs * WS_THREADS >= WS_NB * WS_REG_B + WS_NS * WS_REG_S;
     }
+    if (!ok) return cudaErrorNotSupported;
     scan_ws_kernel<DT, LOGN, SUB_D><<<grid, WS_THREADS, smem, st>>>(w);
     return cudaGetLastError();
 }
