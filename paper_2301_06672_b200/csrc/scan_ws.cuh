@@ -14,13 +14,16 @@
 //           min_normal become subnormal and flush to +0), then the code is
 //           min(bits >> (23-m), 255), done two-at-a-time with u16x2 min.
 //      f16: cvt.rn.satfinite.f16x2.f32 (= RNE of min(x, 65504)).
-//  * 12 SCANNER warps (3 warpgroups, setmaxnreg 48) stream 32-vector code
+//  * 11 SCANNER warps (+ the prep warp: 3 warpgroups, setmaxnreg 48) stream 32-vector code
 //    blocks (16-byte non-allocating loads, interleaved layout) and look the
 //    codes up in the slot's LUTs; R accumulates sequentially in j (fp32).
-//  * builders and scanners exchange LUT slots (NBUF of them, each holding the
-//    LUTs of G probed lists of one query) through mbarriers: full[] (256
-//    builder arrivals) and empty[] (one arrival per scanner warp), so building
-//    job i+1 overlaps scanning job i and scanner warps never wait on each other.
+//  * one PREP warp hands out queries, resolves probe keys 32 at a time and
+//    writes job descriptors + residuals into the slots ahead of the builders;
+//  * prep, builders and scanners exchange LUT slots (NBUF of them, each
+//    holding the LUTs of G probed lists of one query) through mbarriers:
+//    prep[] (1 arrival), full[] (256 builder arrivals) and empty[] (one
+//    arrival per scanner warp), so preparing job i+2, building job i+1 and
+//    scanning job i overlap and scanner warps never wait on each other.
 //  * top-k: each scanner warp filters against the query's shared threshold and
 //    appends survivors to a private smem buffer; a full buffer is rank-sorted
 //    and merged into the query's shared sorted list under a per-query lock.
@@ -34,9 +37,10 @@
 namespace ivfpq {
 
 constexpr int WS_BW = 8;                     // builder warps
-constexpr int WS_SW = 12;                    // scanner warps
+constexpr int WS_SW = 11;                    // scanner warps (+1 prep warp = 3 warpgroups)
 constexpr int WS_NB = WS_BW * 32;            // 256 builder threads
-constexpr int WS_THREADS = (WS_BW + WS_SW) * 32;
+constexpr int WS_PREP_WARP = WS_BW + WS_SW;   // warp 19: job preparation (in the last scanner warpgroup)
+constexpr int WS_THREADS = (WS_BW + WS_SW + 1) * 32;
 constexpr int WS_MAX_G = 8;
 constexpr int WS_MAX_NBUF = 3;
 constexpr int WS_WBUF = 64;                  // per-warp candidate buffer
@@ -48,7 +52,7 @@ constexpr int WS_BAR_BUILD = 1;              // named barrier id for builders
 // checks cudaFuncAttributes::numRegs before using this kernel).
 constexpr int WS_REG_B = 168;
 constexpr int WS_REG_S = 48;
-constexpr int WS_NS = WS_SW * 32;
+constexpr int WS_NS = (WS_SW + 1) * 32;        // threads that run setmaxnreg.dec
 
 struct WsArgs {
     ScanArgs a;            // inputs/outputs shared with the v1 kernel
@@ -62,6 +66,12 @@ struct WsJob {
     int len[WS_MAX_G];
     int lc[WS_MAX_G];
     long long off[WS_MAX_G];
+};
+
+struct WsPrepQ {  // prep warp's queue of resolved probes (<= 32 + G pending)
+    int lc[32 + WS_MAX_G];
+    int len[32 + WS_MAX_G];
+    long long off[32 + WS_MAX_G];
 };
 
 struct WsQuery {
@@ -139,11 +149,14 @@ __device__ __forceinline__ void bar_builders() { asm volatile("bar.sync %0, %1;"
 
 // --------------------------------------------------------------- smem layout
 struct WsLayout {
-    size_t bars, jobs, qst, lists, wbuf, rq, lut, total;
+    size_t bars, jobs, prepq, qst, lists, wbuf, rq, lut, total;
     __host__ __device__ WsLayout(int d, int G, int NBUF, size_t lut_each, int K) {
-        bars = 0;                                                        // full[NBUF], empty[NBUF]
-        jobs = 64;                                                       // WsJob[NBUF]
-        qst = jobs + WS_MAX_NBUF * sizeof(WsJob);                        // WsQuery[NBUF+1]
+        bars = 0;                                                        // prep/full/empty[MAX_NBUF]
+        jobs = 3 * WS_MAX_NBUF * 8;                                      // WsJob[NBUF]
+        jobs = (jobs + 15) & ~(size_t)15;
+        prepq = jobs + WS_MAX_NBUF * sizeof(WsJob);
+        prepq = (prepq + 15) & ~(size_t)15;
+        qst = prepq + sizeof(WsPrepQ);                                   // WsQuery[NBUF+1]
         qst = (qst + 15) & ~(size_t)15;
         lists = qst + (WS_MAX_NBUF + 1) * sizeof(WsQuery);               // u64[NBUF+1][2][K]
         lists = (lists + 15) & ~(size_t)15;
@@ -295,23 +308,57 @@ struct WarpTopK {
     }
 };
 
+// Prep warp: one job = up to G pending probes of query q (pq[from .. from+ng)).
+__device__ __forceinline__ void ws_emit_job(const ScanArgs& a, const WsArgs& w, WsJob* jobs, float* rq_all, u64* empty,
+                                            u64* prep, int job, int NBUF, int G, int q, int qs, const WsPrepQ* pq,
+                                            int from, int ng, bool last, int lane) {
+    const int slot = job % NBUF;
+    if (job >= NBUF) mbar_wait(empty + slot, ((job / NBUF) - 1) & 1);
+    WsJob* J = jobs + slot;
+    if (lane == 0) {
+        int pref = 0;
+        for (int g = 0; g < ng; ++g) {
+            J->lc[g] = pq->lc[from + g];
+            J->len[g] = pq->len[from + g];
+            J->off[g] = pq->off[from + g];
+            J->pref[g] = pref;
+            pref += (pq->len[from + g] + 31) >> 5;
+        }
+        J->pref[ng] = pref;
+        J->nblk = pref;
+        J->ng = ng;
+        J->q = q;
+        J->qs = qs;
+        J->last = last ? 1 : 0;
+    }
+    float* rq = rq_all + (size_t)slot * G * a.d;
+    for (int g = 0; g < ng; ++g) {
+        const float* qv = a.queries + (size_t)q * a.d;
+        const float* cv = a.coarse + (size_t)pq->lc[from + g] * a.d;
+        for (int x = lane; x < a.d; x += 32) rq[g * a.d + x] = __fsub_rn(__ldg(qv + x), __ldg(cv + x));
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(prep + slot);
+}
+
 template <int DT, int LOGN, int SUB_D>
 __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) {
     using T = typename LutTraits<DT>::T;
-    constexpr int N = 1 << LOGN;
     extern __shared__ __align__(16) uint8_t smem[];
     const ScanArgs& a = w.a;
     const int G = a.G, NBUF = w.NBUF, K = a.K, NQS = NBUF + 1;
     const int lut_elems = a.s << LOGN;
     const size_t lut_each = ((size_t)lut_elems * sizeof(T) + 15) & ~(size_t)15;
     const WsLayout L(a.d, G, NBUF, (size_t)lut_elems * sizeof(T), K);
-    u64* full = reinterpret_cast<u64*>(smem + L.bars);
-    u64* empty = full + WS_MAX_NBUF;
+    u64* prep = reinterpret_cast<u64*>(smem + L.bars);   // prep[NBUF]: job + residuals ready
+    u64* full = prep + WS_MAX_NBUF;                       // full[NBUF]: LUTs ready
+    u64* empty = full + WS_MAX_NBUF;                      // empty[NBUF]: slot free
     WsJob* jobs = reinterpret_cast<WsJob*>(smem + L.jobs);
     WsQuery* qst = reinterpret_cast<WsQuery*>(smem + L.qst);
     u64* lists = reinterpret_cast<u64*>(smem + L.lists);
     float* rq_all = reinterpret_cast<float*>(smem + L.rq);
     uint8_t* lut_all = smem + L.lut;
+    WsPrepQ* pq = reinterpret_cast<WsPrepQ*>(smem + L.prepq);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     // ---- setup
@@ -327,6 +374,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
     }
     if (threadIdx.x == 0) {
         for (int b = 0; b < NBUF; ++b) {
+            mbar_init(prep + b, 1);
             mbar_init(full + b, WS_NB);
             mbar_init(empty + b, WS_SW);
         }
@@ -334,83 +382,114 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
     }
     __syncthreads();
 
-    if (warp < WS_BW) {
+    if (warp >= WS_BW) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(WS_REG_S));
+    if (warp == WS_PREP_WARP) {
+        // ============================ prep warp ============================
+        // Hands out queries, resolves probe keys to (local list, offset,
+        // length) 32 at a time, and writes job descriptors + residuals
+        // rq = fl(q - coarse[c]) into the slots, one job ahead of the builders.
+        int job = 0, qseq = -1;
+        while (true) {
+            int q = 0;
+            if (lane == 0) q = atomicAdd(w.work, 1);
+            q = __shfl_sync(0xffffffffu, q, 0);
+            if (q >= a.nq) {
+                const int slot = job % NBUF;
+                if (job >= NBUF) mbar_wait(empty + slot, ((job / NBUF) - 1) & 1);
+                if (lane == 0) {
+                    jobs[slot].qs = -1;
+                    mbar_arrive(prep + slot);
+                }
+                break;
+            }
+            ++qseq;
+            const int qs = qseq % NQS;
+            WsQuery* S = qst + qs;
+            if (lane == 0) {
+                S->q = q;
+                S->ncand = 0;
+            }
+            const u64* probes = a.probes + (size_t)q * a.P;
+            int nq_pend = 0;  // valid probes waiting in pq (warp-uniform)
+            for (int base = 0; base < a.P; base += 32) {
+                const int pi = base + lane;
+                u64 key = pi < a.P ? probes[pi] : ~0ull;
+                const uint32_t gid = (uint32_t)key;
+                const int lc = key == ~0ull ? -1 : a.g2l[gid];
+                long long o = 0, len = 0, gl = 0;
+                if (key != ~0ull) gl = a.glen[gid];
+                if (lc >= 0) {
+                    o = a.off[lc];
+                    len = a.off[lc + 1] - o;
+                }
+                // candidate count of every probe, owned or not
+                for (int sh = 16; sh; sh >>= 1) gl += __shfl_xor_sync(0xffffffffu, gl, sh);
+                if (lane == 0) S->ncand += gl;
+                const bool valid = len > 0;
+                const unsigned m = __ballot_sync(0xffffffffu, valid);
+                if (valid) {
+                    const int at = nq_pend + __popc(m & ((1u << lane) - 1));
+                    pq->lc[at] = lc;
+                    pq->len[at] = (int)len;
+                    pq->off[at] = o;
+                }
+                nq_pend += __popc(m);
+                __syncwarp();
+                const bool more = base + 32 < a.P;
+                // emit full jobs; keep >= 1 pending so the final job knows it is last
+                int taken = 0;
+                while (nq_pend - taken > G || (!more && nq_pend - taken > 0)) {
+                    const int ng = min(G, nq_pend - taken);
+                    const bool last = !more && nq_pend - taken == ng;
+                    ws_emit_job(a, w, jobs, rq_all, empty, prep, job, NBUF, G, q, qs, pq, taken, ng, last, lane);
+                    taken += ng;
+                    ++job;
+                }
+                if (!more && nq_pend == 0) {  // no owned non-empty list: an empty last job
+                    ws_emit_job(a, w, jobs, rq_all, empty, prep, job, NBUF, G, q, qs, pq, 0, 0, true, lane);
+                    ++job;
+                }
+                // compact the pending queue
+                const int rest = nq_pend - taken;
+                int lc2 = 0, len2 = 0;
+                long long o2 = 0;
+                if (lane < rest) {
+                    lc2 = pq->lc[taken + lane];
+                    len2 = pq->len[taken + lane];
+                    o2 = pq->off[taken + lane];
+                }
+                __syncwarp();
+                if (lane < rest) {
+                    pq->lc[lane] = lc2;
+                    pq->len[lane] = len2;
+                    pq->off[lane] = o2;
+                }
+                __syncwarp();
+                nq_pend = rest;
+            }
+        }
+    } else if (warp < WS_BW) {
         // =========================== builders ===========================
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(WS_REG_B));
         const int t = threadIdx.x;
         WsBuild<DT, LOGN, SUB_D> B;
         B.load(a.centers, a.s, t);
-        int q = -1, cursor = a.P, qseq = -1;  // q/cursor/qseq meaningful in thread 0
         for (int job = 0;; ++job) {
             const int slot = job % NBUF;
-            if (job >= NBUF) mbar_wait(empty + slot, ((job / NBUF) - 1) & 1);
-            WsJob* J = jobs + slot;
-            if (t == 0) {
-                // next job: up to G valid probes of the current query, or a new query
-                if (cursor >= a.P) {
-                    q = atomicAdd(w.work, 1);
-                    cursor = 0;
-                    ++qseq;
-                    if (q < a.nq) {
-                        WsQuery* S = qst + (qseq % NQS);
-                        S->q = q;
-                        S->ncand = 0;
-                    }
-                }
-                if (q >= a.nq) {
-                    J->qs = -1;
-                } else {
-                    WsQuery* S = qst + (qseq % NQS);
-                    const u64* probes = a.probes + (size_t)q * a.P;
-                    int ng = 0, pref = 0;
-                    long long nc = 0;
-                    while (cursor < a.P) {
-                        const u64 key = probes[cursor];
-                        const uint32_t gid = (uint32_t)key;
-                        const int lc = key == ~0ull ? -1 : a.g2l[gid];
-                        const long long o = lc >= 0 ? a.off[lc] : 0;
-                        const long long len = lc >= 0 ? a.off[lc + 1] - o : 0;
-                        if (len > 0 && ng == G) break;   // next job starts here
-                        ++cursor;
-                        if (key != ~0ull) nc += a.glen[gid];
-                        if (len == 0) continue;
-                        J->lc[ng] = lc;
-                        J->len[ng] = (int)len;
-                        J->off[ng] = o;
-                        J->pref[ng] = pref;
-                        pref += (int)((len + 31) >> 5);
-                        ++ng;
-                    }
-                    S->ncand += nc;
-                    J->qs = qseq % NQS;
-                    J->q = q;
-                    J->ng = ng;
-                    J->pref[ng] = pref;
-                    J->nblk = pref;
-                    J->last = cursor >= a.P;
-                }
-            }
-            bar_builders();
-            const int qs = J->qs;
-            if (qs < 0) {
+            mbar_wait(prep + slot, (job / NBUF) & 1);
+            const WsJob* J = jobs + slot;
+            if (J->qs < 0) {
                 mbar_arrive(full + slot);
                 break;
             }
-            const int ng = J->ng, jq = J->q;
-            float* rq = rq_all + (size_t)slot * G * a.d;
-            for (int i = t; i < ng * a.d; i += WS_NB) {
-                const int g = i / a.d, x = i - g * a.d;
-                rq[i] = __fsub_rn(__ldg(a.queries + (size_t)jq * a.d + x), __ldg(a.coarse + (size_t)J->lc[g] * a.d + x));
-            }
-            bar_builders();
-            T* lut = reinterpret_cast<T*>(lut_all + (size_t)slot * G * lut_each);
-            for (int g = 0; g < ng; ++g)
-                B.build(rq + (size_t)g * a.d, reinterpret_cast<T*>(reinterpret_cast<uint8_t*>(lut) + g * lut_each), a.s);
+            const int ng = J->ng;
+            const float* rq = rq_all + (size_t)slot * G * a.d;
+            uint8_t* lut = lut_all + (size_t)slot * G * lut_each;
+            for (int g = 0; g < ng; ++g) B.build(rq + (size_t)g * a.d, reinterpret_cast<T*>(lut + g * lut_each), a.s);
             mbar_arrive(full + slot);
         }
     } else {
         // =========================== scanners ===========================
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(WS_REG_S));
         const int sw = warp - WS_BW;
         u64* wb = reinterpret_cast<u64*>(smem + L.wbuf) + (size_t)sw * 2 * WS_WBUF;
         WarpTopK tk{wb, wb + WS_WBUF, 0};
