@@ -387,12 +387,14 @@ bool ws_plan(const ivfpq_index* idx, int64_t P, int64_t K, int dt, WsPlan* plan)
     const int64_t R = 1024 / N;
     const int64_t jpt = 32 / idx->sub_d;
     if ((idx->s + R - 1) / R > jpt) return false;
-    const size_t lut_each = (size_t)idx->s * N * lut_bytes_of((int)dt);
+    const size_t lut_each = WsLayout((int)idx->d, (int)idx->s, (int)idx->sub_d, (int)idx->p, lut_bytes_of((int)dt), 1,
+                                     2, (int)K).lut_each;
     int G = (int)std::max<size_t>(1, std::min<size_t>(WS_MAX_G, lut_budget_bytes() / lut_each));
     G = (int)std::min<int64_t>(G, std::max<int64_t>(1, P));
     for (; G >= 1; --G)
         for (int nb = WS_MAX_NBUF; nb >= 2; --nb) {
-            const size_t sm = WsLayout((int)idx->d, G, nb, lut_each, (int)K).total;
+            const size_t sm = WsLayout((int)idx->d, (int)idx->s, (int)idx->sub_d, (int)idx->p, lut_bytes_of((int)dt), G,
+                                       nb, (int)K).total;
             if (sm <= SMEM_LIMIT) {
                 *plan = WsPlan{G, nb, sm};
                 return true;

@@ -43,6 +43,7 @@ constexpr int WS_PREP_WARP = WS_BW + WS_SW;   // warp 19: job preparation (in th
 constexpr int WS_THREADS = (WS_BW + WS_SW + 1) * 32;
 constexpr int WS_MAX_G = 8;
 constexpr int WS_MAX_NBUF = 3;
+constexpr int WS_PD = 8;                     // prep ring depth (jobs prepared ahead)
 constexpr int WS_WBUF = 64;                  // per-warp candidate buffer
 constexpr int WS_MAX_K = 512;
 constexpr int WS_BAR_BUILD = 1;              // named barrier id for builders
@@ -145,25 +146,48 @@ __device__ __forceinline__ void mbar_wait(u64* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
-__device__ __forceinline__ void bar_builders() { asm volatile("bar.sync %0, %1;" ::"n"(WS_BAR_BUILD), "n"(WS_NB) : "memory"); }
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void lds_f32x2(uint32_t a, float& x, float& y) {
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(x), "=f"(y) : "r"(a));
+}
+__device__ __forceinline__ void lds_f32x4(uint32_t a, float& x, float& y, float& z, float& w) {
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(x), "=f"(y), "=f"(z), "=f"(w) : "r"(a));
+}
+__device__ __forceinline__ void sts_b32(uint32_t a, uint32_t v) { asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v)); }
+__device__ __forceinline__ void sts_v2(uint32_t a, uint32_t x, uint32_t y) {
+    asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(a), "r"(x), "r"(y));
+}
+__device__ __forceinline__ void sts_v4f(uint32_t a, float x, float y, float z, float w) {
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(x), "f"(y), "f"(z), "f"(w));
+}
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 // --------------------------------------------------------------- smem layout
 struct WsLayout {
-    size_t bars, jobs, prepq, qst, lists, wbuf, rq, lut, total;
-    __host__ __device__ WsLayout(int d, int G, int NBUF, size_t lut_each, int K) {
-        bars = 0;                                                        // prep/full/empty[MAX_NBUF]
-        jobs = 3 * WS_MAX_NBUF * 8;                                      // WsJob[NBUF]
-        jobs = (jobs + 15) & ~(size_t)15;
-        prepq = jobs + WS_MAX_NBUF * sizeof(WsJob);
+    // lut rows are padded to R * jpt (jpt = ceil(s / R)) so every builder
+    // thread runs the same number of rows; rq vectors likewise to R*jpt*sub_d.
+    size_t bars, jobs, pjobs, prepq, qst, lists, wbuf, prq, lut, total, lut_each, d_pad;
+    __host__ __device__ WsLayout(int d, int s, int sub_d, int logn, int esize, int G, int NBUF, int K) {
+        const int N = 1 << logn, R = 1024 / N, jpt = (s + R - 1) / R;
+        lut_each = (((size_t)R * jpt * N * esize) + 15) & ~(size_t)15;
+        d_pad = (size_t)R * jpt * sub_d;
+        bars = 0;                                                         // pfull/pempty[PD], full/empty[MAX_NBUF]
+        jobs = (2 * WS_PD + 2 * WS_MAX_NBUF) * 8;                        // WsJob[MAX_NBUF] (LUT slots)
+        pjobs = jobs + WS_MAX_NBUF * sizeof(WsJob);                       // WsJob[PD] (prep ring)
+        prepq = pjobs + WS_PD * sizeof(WsJob);
         prepq = (prepq + 15) & ~(size_t)15;
-        qst = prepq + sizeof(WsPrepQ);                                   // WsQuery[NBUF+1]
+        qst = prepq + sizeof(WsPrepQ);                                    // WsQuery[MAX_NBUF+1]
         qst = (qst + 15) & ~(size_t)15;
-        lists = qst + (WS_MAX_NBUF + 1) * sizeof(WsQuery);               // u64[NBUF+1][2][K]
+        lists = qst + (WS_MAX_NBUF + 1) * sizeof(WsQuery);                // u64[NBUF+1][2][K]
         lists = (lists + 15) & ~(size_t)15;
-        wbuf = lists + (size_t)(NBUF + 1) * 2 * K * 8;                   // u64[SW][2][WBUF]
-        rq = wbuf + (size_t)WS_SW * 2 * WS_WBUF * 8;                     // f32[NBUF][G][d]
-        lut = rq + (((size_t)NBUF * G * d * 4 + 15) & ~(size_t)15);      // [NBUF][G][lut_each]
-        total = lut + (size_t)NBUF * G * ((lut_each + 15) & ~(size_t)15);
+        wbuf = lists + (size_t)(NBUF + 1) * 2 * K * 8;                    // u64[SW][2][WBUF]
+        prq = wbuf + (size_t)WS_SW * 2 * WS_WBUF * 8;                     // f32[PD][G][d_pad]
+        lut = prq + (((size_t)WS_PD * G * d_pad * 4 + 15) & ~(size_t)15); // [NBUF][G][lut_each]
+        total = lut + (size_t)NBUF * G * lut_each;
     }
 };
 
@@ -201,39 +225,51 @@ struct WsBuild {
         }
     }
 
-    // One table (one probed list): rq[d] in smem -> lut (s x N entries) in smem.
-    __device__ __forceinline__ void build(const float* rq, T* lut, int s) const {
+    // One table: rq (smem, d_pad floats) -> LUT (smem, R*jpt rows of N).
+    // Shared addresses are 32-bit bases + compile-time offsets; jpt is the
+    // same for every thread (rows padded), so the only branch is the exit.
+    __device__ __forceinline__ void build(uint32_t rq_s, uint32_t lut_s, int jpt) const {
+        constexpr int E = sizeof(T);
+        const uint32_t rqb = rq_s + (uint32_t)jr * SUB_D * 4;
+        const uint32_t lb = lut_s + ((uint32_t)jr * N + 4 * u) * E;
 #pragma unroll
         for (int i = 0; i < JPT; ++i) {
-            const int j = jr + R * i;
-            if (j < s) {
-                u64 acc0 = 0, acc1 = 0;
+            if (i >= jpt) break;
+            float r[SUB_D];
+            const uint32_t ra = rqb + i * R * SUB_D * 4;
+            if constexpr (SUB_D == 2) {
+                lds_f32x2(ra, r[0], r[1]);
+            } else if constexpr (SUB_D == 4) {
+                lds_f32x4(ra, r[0], r[1], r[2], r[3]);
+            } else {
 #pragma unroll
-                for (int x = 0; x < SUB_D; ++x) {
-                    const float r = rq[j * SUB_D + x];
-                    const u64 rr = pk2(r, r);
-                    const u64 d0 = sub2(cen[i][0][x], rr), d1 = sub2(cen[i][1][x], rr);
-                    const u64 q0 = mul2(d0, d0), q1 = mul2(d1, d1);
-                    // acc starts at +0: fl(0 + q) = q exactly (q >= +0)
-                    acc0 = x == 0 ? q0 : add2(acc0, q0);
-                    acc1 = x == 0 ? q1 : add2(acc1, q1);
-                }
-                store(lut + (size_t)j * N + 4 * u, acc0, acc1);
+                for (int x = 0; x < SUB_D; ++x) r[x] = lds_f32(ra + 4 * x);
             }
+            u64 acc0 = 0, acc1 = 0;
+#pragma unroll
+            for (int x = 0; x < SUB_D; ++x) {
+                const u64 rr = pk2(r[x], r[x]);
+                const u64 d0 = sub2(cen[i][0][x], rr), d1 = sub2(cen[i][1][x], rr);
+                const u64 q0 = mul2(d0, d0), q1 = mul2(d1, d1);
+                // acc starts at +0: fl(0 + q) = q exactly (q >= +0)
+                acc0 = x == 0 ? q0 : add2(acc0, q0);
+                acc1 = x == 0 ? q1 : add2(acc1, q1);
+            }
+            store(lb + i * R * N * E, acc0, acc1);
         }
     }
 
-    __device__ __forceinline__ static void store(T* dst, u64 a01, u64 a23) {
+    __device__ __forceinline__ static void store(uint32_t dst, u64 a01, u64 a23) {
         if constexpr (DT == LUT_F32) {
             float a0, a1, a2, a3;
             upk2(a01, a0, a1);
             upk2(a23, a2, a3);
-            *reinterpret_cast<float4*>(dst) = make_float4(a0, a1, a2, a3);
+            sts_v4f(dst, a0, a1, a2, a3);
         } else if constexpr (DT == LUT_F16) {
             float a0, a1, a2, a3;
             upk2(a01, a0, a1);
             upk2(a23, a2, a3);
-            *reinterpret_cast<uint2*>(dst) = make_uint2(cvt_f16x2_sat(a0, a1), cvt_f16x2_sat(a2, a3));
+            sts_v2(dst, cvt_f16x2_sat(a0, a1), cvt_f16x2_sat(a2, a3));
         } else {
             constexpr int M = LutTraits<DT>::m, BIAS = LutTraits<DT>::bias;
             // y = x * 2^-(127-bias), round-toward-zero + flush-to-zero: exact
@@ -250,7 +286,7 @@ struct WsBuild {
             uint32_t h23 = __byte_perm(__float_as_uint(f2), __float_as_uint(f3), 0x7632);
             h01 = min_u16x2(h01, lim | (lim << 16)) >> (7 - M);
             h23 = min_u16x2(h23, lim | (lim << 16)) >> (7 - M);
-            *reinterpret_cast<uint32_t*>(dst) = __byte_perm(h01, h23, 0x6420);
+            sts_b32(dst, __byte_perm(h01, h23, 0x6420));
         }
     }
 };
@@ -308,13 +344,14 @@ struct WarpTopK {
     }
 };
 
-// Prep warp: one job = up to G pending probes of query q (pq[from .. from+ng)).
-__device__ __forceinline__ void ws_emit_job(const ScanArgs& a, const WsArgs& w, WsJob* jobs, float* rq_all, u64* empty,
-                                            u64* prep, int job, int NBUF, int G, int q, int qs, const WsPrepQ* pq,
-                                            int from, int ng, bool last, int lane) {
-    const int slot = job % NBUF;
-    if (job >= NBUF) mbar_wait(empty + slot, ((job / NBUF) - 1) & 1);
-    WsJob* J = jobs + slot;
+// Prep warp: one job = up to G pending probes of query q (pq[from .. from+ng))
+// written into prep-ring entry job % PD (descriptor + padded residuals).
+__device__ __forceinline__ void ws_emit_job(const ScanArgs& a, WsJob* pjobs, float* prq, u64* pfull, u64* pempty,
+                                            int job, int G, int d_pad, int q, int qs, const WsPrepQ* pq, int from,
+                                            int ng, bool last, int lane) {
+    const int ps = job % WS_PD;
+    if (job >= WS_PD) mbar_wait(pempty + ps, ((job / WS_PD) - 1) & 1);
+    WsJob* J = pjobs + ps;
     if (lane == 0) {
         int pref = 0;
         for (int g = 0; g < ng; ++g) {
@@ -331,14 +368,15 @@ __device__ __forceinline__ void ws_emit_job(const ScanArgs& a, const WsArgs& w, 
         J->qs = qs;
         J->last = last ? 1 : 0;
     }
-    float* rq = rq_all + (size_t)slot * G * a.d;
+    float* rq = prq + (size_t)ps * G * d_pad;
+    const float* qv = a.queries + (size_t)q * a.d;
     for (int g = 0; g < ng; ++g) {
-        const float* qv = a.queries + (size_t)q * a.d;
         const float* cv = a.coarse + (size_t)pq->lc[from + g] * a.d;
-        for (int x = lane; x < a.d; x += 32) rq[g * a.d + x] = __fsub_rn(__ldg(qv + x), __ldg(cv + x));
+        for (int x = lane; x < d_pad; x += 32)
+            rq[g * d_pad + x] = x < a.d ? __fsub_rn(__ldg(qv + x), __ldg(cv + x)) : 0.0f;
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(prep + slot);
+    if (lane == 0) mbar_arrive(pfull + ps);
 }
 
 template <int DT, int LOGN, int SUB_D>
@@ -347,16 +385,19 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
     extern __shared__ __align__(16) uint8_t smem[];
     const ScanArgs& a = w.a;
     const int G = a.G, NBUF = w.NBUF, K = a.K, NQS = NBUF + 1;
-    const int lut_elems = a.s << LOGN;
-    const size_t lut_each = ((size_t)lut_elems * sizeof(T) + 15) & ~(size_t)15;
-    const WsLayout L(a.d, G, NBUF, (size_t)lut_elems * sizeof(T), K);
-    u64* prep = reinterpret_cast<u64*>(smem + L.bars);   // prep[NBUF]: job + residuals ready
-    u64* full = prep + WS_MAX_NBUF;                       // full[NBUF]: LUTs ready
-    u64* empty = full + WS_MAX_NBUF;                      // empty[NBUF]: slot free
+    const WsLayout L(a.d, a.s, SUB_D, LOGN, (int)sizeof(T), G, NBUF, K);
+    const size_t lut_each = L.lut_each;
+    const int d_pad = (int)L.d_pad;
+    const int jpt = (a.s + WsBuild<DT, LOGN, SUB_D>::R - 1) / WsBuild<DT, LOGN, SUB_D>::R;
+    u64* pfull = reinterpret_cast<u64*>(smem + L.bars);  // pfull[PD]: job + residuals prepared
+    u64* pempty = pfull + WS_PD;                          // pempty[PD]: prep entry consumed
+    u64* full = pempty + WS_PD;                           // full[NBUF]: LUTs ready
+    u64* empty = full + WS_MAX_NBUF;                      // empty[NBUF]: LUT slot free
     WsJob* jobs = reinterpret_cast<WsJob*>(smem + L.jobs);
+    WsJob* pjobs = reinterpret_cast<WsJob*>(smem + L.pjobs);
     WsQuery* qst = reinterpret_cast<WsQuery*>(smem + L.qst);
     u64* lists = reinterpret_cast<u64*>(smem + L.lists);
-    float* rq_all = reinterpret_cast<float*>(smem + L.rq);
+    float* prq = reinterpret_cast<float*>(smem + L.prq);
     uint8_t* lut_all = smem + L.lut;
     WsPrepQ* pq = reinterpret_cast<WsPrepQ*>(smem + L.prepq);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -373,8 +414,11 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
         S->q = -1;
     }
     if (threadIdx.x == 0) {
+        for (int b = 0; b < WS_PD; ++b) {
+            mbar_init(pfull + b, 1);
+            mbar_init(pempty + b, WS_NB);
+        }
         for (int b = 0; b < NBUF; ++b) {
-            mbar_init(prep + b, 1);
             mbar_init(full + b, WS_NB);
             mbar_init(empty + b, WS_SW);
         }
@@ -394,11 +438,11 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
             if (lane == 0) q = atomicAdd(w.work, 1);
             q = __shfl_sync(0xffffffffu, q, 0);
             if (q >= a.nq) {
-                const int slot = job % NBUF;
-                if (job >= NBUF) mbar_wait(empty + slot, ((job / NBUF) - 1) & 1);
+                const int ps = job % WS_PD;
+                if (job >= WS_PD) mbar_wait(pempty + ps, ((job / WS_PD) - 1) & 1);
                 if (lane == 0) {
-                    jobs[slot].qs = -1;
-                    mbar_arrive(prep + slot);
+                    pjobs[ps].qs = -1;
+                    mbar_arrive(pfull + ps);
                 }
                 break;
             }
@@ -441,12 +485,12 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
                 while (nq_pend - taken > G || (!more && nq_pend - taken > 0)) {
                     const int ng = min(G, nq_pend - taken);
                     const bool last = !more && nq_pend - taken == ng;
-                    ws_emit_job(a, w, jobs, rq_all, empty, prep, job, NBUF, G, q, qs, pq, taken, ng, last, lane);
+                    ws_emit_job(a, pjobs, prq, pfull, pempty, job, G, d_pad, q, qs, pq, taken, ng, last, lane);
                     taken += ng;
                     ++job;
                 }
                 if (!more && nq_pend == 0) {  // no owned non-empty list: an empty last job
-                    ws_emit_job(a, w, jobs, rq_all, empty, prep, job, NBUF, G, q, qs, pq, 0, 0, true, lane);
+                    ws_emit_job(a, pjobs, prq, pfull, pempty, job, G, d_pad, q, qs, pq, 0, 0, true, lane);
                     ++job;
                 }
                 // compact the pending queue
@@ -474,18 +518,25 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
         const int t = threadIdx.x;
         WsBuild<DT, LOGN, SUB_D> B;
         B.load(a.centers, a.s, t);
+        const uint32_t prq_s = smem_addr(prq), lut_s = smem_addr(lut_all);
         for (int job = 0;; ++job) {
-            const int slot = job % NBUF;
-            mbar_wait(prep + slot, (job / NBUF) & 1);
-            const WsJob* J = jobs + slot;
-            if (J->qs < 0) {
+            const int ps = job % WS_PD, slot = job % NBUF;
+            mbar_wait(pfull + ps, (job / WS_PD) & 1);
+            if (job >= NBUF) mbar_wait(empty + slot, ((job / NBUF) - 1) & 1);
+            const WsJob* PJ = pjobs + ps;
+            if (t < 32) {  // the descriptor travels with the LUT slot (warp 0 copies it)
+                const int* src = reinterpret_cast<const int*>(PJ);
+                int* dst = reinterpret_cast<int*>(jobs + slot);
+                for (int i = t; i < (int)(sizeof(WsJob) / 4); i += 32) dst[i] = src[i];
+            }
+            if (PJ->qs < 0) {
                 mbar_arrive(full + slot);
                 break;
             }
-            const int ng = J->ng;
-            const float* rq = rq_all + (size_t)slot * G * a.d;
-            uint8_t* lut = lut_all + (size_t)slot * G * lut_each;
-            for (int g = 0; g < ng; ++g) B.build(rq + (size_t)g * a.d, reinterpret_cast<T*>(lut + g * lut_each), a.s);
+            const int ng = PJ->ng;
+            for (int g = 0; g < ng; ++g)
+                B.build(prq_s + (uint32_t)((ps * G + g) * d_pad * 4), lut_s + (uint32_t)((slot * G + g) * lut_each), jpt);
+            mbar_arrive(pempty + ps);
             mbar_arrive(full + slot);
         }
     } else {
@@ -502,7 +553,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
             WsQuery* S = qst + qs;
             u64* qlist = lists + (size_t)qs * 2 * K;
             const int ng = J->ng, nblk = J->nblk;
-            const uint8_t* lutb = lut_all + (size_t)slot * G * lut_each;
+            const uint8_t* lutb = lut_all + (size_t)slot * G * lut_each;  // rows padded; scan reads j < s
             for (int b = sw; b < nblk; b += WS_SW) {
                 int g = 0;
                 while (g + 1 < ng && b >= J->pref[g + 1]) ++g;
@@ -525,8 +576,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
                 tk.offer(key, pass);
                 if (tk.n > WS_WBUF - 32) tk.flush(S, qlist, K);
             }
-            if (tk.n > 0) tk.flush(S, qlist, K);
             if (J->last) {
+                if (tk.n > 0) tk.flush(S, qlist, K);
                 int d = 0;
                 if (lane == 0) d = atomicAdd(&S->done, 1);
                 d = __shfl_sync(0xffffffffu, d, 0);
