@@ -4,17 +4,19 @@
 // scan_list :130-142, top_k :145-155) and as scan.cuh, restructured for B200:
 //
 //  * one CTA per SM (persistent), queries handed out by a global atomic;
-//  * 8 BUILDER warps (2 warpgroups, setmaxnreg 168) keep the whole PQ codebook
-//    in registers: builder thread t owns a quad of codes m = 4u..4u+3 and the
-//    subspaces j = jr, jr+R, ... (u = t % (N/4), jr = t / (N/4), R = 1024/N).
-//    Per (j, quad) one broadcast read of rq[j] feeds 4 table entries computed
+//  * the whole PQ codebook lives in TENSOR MEMORY (128 KiB of the SM's 256 KiB
+//    TMEM, tcgen05.alloc/st/ld): 8 BUILDER warps each read only their own
+//    lane's columns: builder thread t owns a quad of codes m = 4u..4u+3 and
+//    the subspaces j = jr, jr+R, ... (u = t % (N/4), jr = t / (N/4),
+//    R = 1024/N); one tcgen05.ld of a row's centers serves all G lists of a
+//    job.  Per (j, quad) one broadcast read of rq[j] feeds 4 table entries computed
 //    with packed f32x2 sub/mul/add (exact: every op is one IEEE rounding, in
 //    the reference order), then stored with one 4-, 8- or 16-byte STS:
 //      fp8: mul.rz.ftz.f32x2 by 2^-(127-bias) (exact scaling; values below
 //           min_normal become subnormal and flush to +0), then the code is
 //           min(bits >> (23-m), 255), done two-at-a-time with u16x2 min.
 //      f16: cvt.rn.satfinite.f16x2.f32 (= RNE of min(x, 65504)).
-//  * 11 SCANNER warps (+ the prep warp: 3 warpgroups, setmaxnreg 48) stream 32-vector code
+//  * 11 SCANNER warps stream 32-vector code
 //    blocks (16-byte non-allocating loads, interleaved layout) and look the
 //    codes up in the slot's LUTs; R accumulates sequentially in j (fp32).
 //  * one PREP warp hands out queries, resolves probe keys 32 at a time and
@@ -47,13 +49,7 @@ constexpr int WS_PD = 8;                     // prep ring depth (jobs prepared a
 constexpr int WS_WBUF = 64;                  // per-warp candidate buffer
 constexpr int WS_MAX_K = 512;
 constexpr int WS_BAR_BUILD = 1;              // named barrier id for builders
-// setmaxnreg budget: .inc draws only on registers released by .dec inside the
-// CTA, so WS_NB*WS_REG_B + WS_NS*WS_REG_S must not exceed the launch
-// allocation WS_THREADS * regs (ptxas gives 96 at 640 threads; the host
-// checks cudaFuncAttributes::numRegs before using this kernel).
-constexpr int WS_REG_B = 168;
-constexpr int WS_REG_S = 48;
-constexpr int WS_NS = (WS_SW + 1) * 32;        // threads that run setmaxnreg.dec
+
 
 struct WsArgs {
     ScanArgs a;            // inputs/outputs shared with the v1 kernel
@@ -146,6 +142,7 @@ __device__ __forceinline__ void mbar_wait(u64* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+__device__ __forceinline__ void bar_builders() { asm volatile("bar.sync %0, %1;" ::"n"(WS_BAR_BUILD), "n"(WS_NB) : "memory"); }
 __device__ __forceinline__ float lds_f32(uint32_t a) {
     float v;
     asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
@@ -166,17 +163,72 @@ __device__ __forceinline__ void sts_v4f(uint32_t a, float x, float y, float z, f
 }
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
+// ---- tensor memory (TMEM): the codebook lives here, one 32-bit column per
+// float, builder thread (w, i) in lane 32*(w%4)+i, column half w/4.
+template <int NCOL>
+__device__ __forceinline__ void tmem_alloc(uint32_t dst_smem) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(dst_smem), "n"(NCOL));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+}
+template <int NCOL>
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(NCOL));
+}
+__device__ __forceinline__ void tmem_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+template <int X>
+__device__ __forceinline__ void tmem_ld(uint32_t taddr, uint32_t (&r)[X]) {
+    if constexpr (X == 4) {
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                     : "r"(taddr));
+    } else if constexpr (X == 8) {
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                     : "r"(taddr));
+    } else {
+        static_assert(X == 16, "x4 / x8 / x16 only");
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+            "%15}, [%16];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+            : "r"(taddr));
+    }
+}
+template <int X>
+__device__ __forceinline__ void tmem_st(uint32_t taddr, const uint32_t (&r)[X]) {
+    if constexpr (X == 4) {
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr), "r"(r[0]),
+                     "r"(r[1]), "r"(r[2]), "r"(r[3]));
+    } else if constexpr (X == 8) {
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+                     "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]));
+    } else {
+        static_assert(X == 16, "x4 / x8 / x16 only");
+        asm volatile(
+            "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+            "%15, %16};" ::"r"(taddr),
+            "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+            "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]));
+    }
+}
+
 // --------------------------------------------------------------- smem layout
 struct WsLayout {
     // lut rows are padded to R * jpt (jpt = ceil(s / R)) so every builder
     // thread runs the same number of rows; rq vectors likewise to R*jpt*sub_d.
-    size_t bars, jobs, pjobs, prepq, qst, lists, wbuf, prq, lut, total, lut_each, d_pad;
+    size_t bars, tmem, jobs, pjobs, prepq, qst, lists, wbuf, prq, lut, total, lut_each, d_pad;
     __host__ __device__ WsLayout(int d, int s, int sub_d, int logn, int esize, int G, int NBUF, int K) {
         const int N = 1 << logn, R = 1024 / N, jpt = (s + R - 1) / R;
-        lut_each = (((size_t)R * jpt * N * esize) + 15) & ~(size_t)15;
+        lut_each = (((size_t)R * jpt * N * esize) + 255) & ~(size_t)255;  // 256-aligned (PRMT addressing)
         d_pad = (size_t)R * jpt * sub_d;
         bars = 0;                                                         // pfull/pempty[PD], full/empty[MAX_NBUF]
-        jobs = (2 * WS_PD + 2 * WS_MAX_NBUF) * 8;                        // WsJob[MAX_NBUF] (LUT slots)
+        tmem = (2 * WS_PD + 2 * WS_MAX_NBUF) * 8;                        // u32: TMEM base address
+        jobs = tmem + 16;                                                 // WsJob[MAX_NBUF] (LUT slots)
         pjobs = jobs + WS_MAX_NBUF * sizeof(WsJob);                       // WsJob[PD] (prep ring)
         prepq = pjobs + WS_PD * sizeof(WsJob);
         prepq = (prepq + 15) & ~(size_t)15;
@@ -186,76 +238,101 @@ struct WsLayout {
         lists = (lists + 15) & ~(size_t)15;
         wbuf = lists + (size_t)(NBUF + 1) * 2 * K * 8;                    // u64[SW][2][WBUF]
         prq = wbuf + (size_t)WS_SW * 2 * WS_WBUF * 8;                     // f32[PD][G][d_pad]
-        lut = prq + (((size_t)WS_PD * G * d_pad * 4 + 15) & ~(size_t)15); // [NBUF][G][lut_each]
+        lut = prq + (size_t)WS_PD * G * d_pad * 4;                        // [NBUF][G][lut_each]
+        lut = (lut + 255) & ~(size_t)255;
         total = lut + (size_t)NBUF * G * lut_each;
     }
 };
 
 // ------------------------------------------------------------- the builders
-// JPT: compile-time bound on the subspaces one builder thread owns.
+// Builder thread t owns codes m = 4u..4u+3 (u = t % (N/4)) of subspaces
+// j = jr + R*i (jr = t / (N/4), R = 1024/N), i < jpt.  Its centers live in
+// TMEM: for owned row i, CPI columns hold c[m0..m0+3][0..SUB_D) (pairs packed
+// as (c[m0][x], c[m0+1][x]), (c[m0+2][x], c[m0+3][x])).
 template <int DT, int LOGN, int SUB_D>
 struct WsBuild {
     static constexpr int N = 1 << LOGN;
-    static constexpr int NQ4 = N / 4;               // quads per subspace row
-    static constexpr int R = WS_NB / NQ4;           // row groups
-    static constexpr int JPT = 32 / SUB_D;          // 4 * JPT * SUB_D <= 128 registers
+    static constexpr int NQ4 = N / 4;                                   // quads per subspace row
+    static constexpr int R = WS_NB / NQ4;                               // row groups
+    static constexpr int JPT = 32 / SUB_D;                              // max owned rows (host-checked)
+    static constexpr int CPI = SUB_D == 1 ? 4 : SUB_D == 2 ? 8 : 16;    // TMEM columns per owned row
+    static constexpr int HALF = JPT * CPI;                              // columns per builder half
+    static constexpr int NCOL = 2 * HALF <= 256 ? 256 : 512;            // TMEM allocation
     using T = typename LutTraits<DT>::T;
 
-    u64 cen[JPT][2][SUB_D];  // (c[m0], c[m0+1]) and (c[m0+2], c[m0+3]) per owned j, per dim
     int u, jr;
+    uint32_t tbase;  // this thread's TMEM address (lane quarter | column half)
 
-    __device__ void load(const float* __restrict__ centers, int s, int t) {
+    __device__ void init(const float* __restrict__ centers, int s, int t, uint32_t tmem) {
+        const int w = t >> 5;
         u = t % NQ4;
         jr = t / NQ4;
-#pragma unroll
+        tbase = tmem + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)((w >> 2) * HALF);
+#pragma unroll 1
         for (int i = 0; i < JPT; ++i) {
             const int j = jr + R * i;
+            uint32_t r[CPI];
 #pragma unroll
-            for (int h = 0; h < 2; ++h)
+            for (int k = 0; k < CPI; ++k) r[k] = 0u;
+            if (j < s) {
 #pragma unroll
-                for (int x = 0; x < SUB_D; ++x) {
-                    float a = 0.f, b = 0.f;
-                    if (j < s) {
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                    for (int x = 0; x < SUB_D; ++x) {
                         const size_t e = (size_t)j * N + 4 * u + 2 * h;
-                        a = __ldg(centers + e * SUB_D + x);
-                        b = __ldg(centers + (e + 1) * SUB_D + x);
+                        r[(h * SUB_D + x) * 2 + 0] = __float_as_uint(__ldg(centers + e * SUB_D + x));
+                        r[(h * SUB_D + x) * 2 + 1] = __float_as_uint(__ldg(centers + (e + 1) * SUB_D + x));
                     }
-                    cen[i][h][x] = pk2(a, b);
-                }
+            }
+            tmem_st<CPI>(tbase + i * CPI, r);
         }
+        tmem_wait_st();
     }
 
-    // One table: rq (smem, d_pad floats) -> LUT (smem, R*jpt rows of N).
-    // Shared addresses are 32-bit bases + compile-time offsets; jpt is the
-    // same for every thread (rows padded), so the only branch is the exit.
-    __device__ __forceinline__ void build(uint32_t rq_s, uint32_t lut_s, int jpt) const {
+    // The LUTs of ng lists: rq_s[g] (smem, d_pad floats) -> lut_s[g] (smem,
+    // R*jpt rows of N).  Centers of row i are read from TMEM once and reused
+    // for every list of the job.
+    __device__ __forceinline__ void build(uint32_t rq_s, uint32_t rq_stride, uint32_t lut_s, uint32_t lut_stride,
+                                          int ng, int jpt) const {
         constexpr int E = sizeof(T);
         const uint32_t rqb = rq_s + (uint32_t)jr * SUB_D * 4;
         const uint32_t lb = lut_s + ((uint32_t)jr * N + 4 * u) * E;
+#pragma unroll 1
+        for (int i = 0; i < jpt; ++i) {
+            uint32_t c[CPI];
+            tmem_ld<CPI>(tbase + i * CPI, c);
+            tmem_wait_ld();
+            u64 cen[2][SUB_D];
 #pragma unroll
-        for (int i = 0; i < JPT; ++i) {
-            if (i >= jpt) break;
-            float r[SUB_D];
-            const uint32_t ra = rqb + i * R * SUB_D * 4;
-            if constexpr (SUB_D == 2) {
-                lds_f32x2(ra, r[0], r[1]);
-            } else if constexpr (SUB_D == 4) {
-                lds_f32x4(ra, r[0], r[1], r[2], r[3]);
-            } else {
+            for (int h = 0; h < 2; ++h)
 #pragma unroll
-                for (int x = 0; x < SUB_D; ++x) r[x] = lds_f32(ra + 4 * x);
+                for (int x = 0; x < SUB_D; ++x)
+                    cen[h][x] = pk2(__uint_as_float(c[(h * SUB_D + x) * 2]), __uint_as_float(c[(h * SUB_D + x) * 2 + 1]));
+            const uint32_t ra0 = rqb + i * R * SUB_D * 4, la0 = lb + i * R * N * E;
+#pragma unroll 4
+            for (int g = 0; g < ng; ++g) {
+                float r[SUB_D];
+                const uint32_t ra = ra0 + g * rq_stride;
+                if constexpr (SUB_D == 2) {
+                    lds_f32x2(ra, r[0], r[1]);
+                } else if constexpr (SUB_D == 4) {
+                    lds_f32x4(ra, r[0], r[1], r[2], r[3]);
+                } else {
+#pragma unroll
+                    for (int x = 0; x < SUB_D; ++x) r[x] = lds_f32(ra + 4 * x);
+                }
+                u64 acc0 = 0, acc1 = 0;
+#pragma unroll
+                for (int x = 0; x < SUB_D; ++x) {
+                    const u64 rr = pk2(r[x], r[x]);
+                    const u64 d0 = sub2(cen[0][x], rr), d1 = sub2(cen[1][x], rr);
+                    const u64 q0 = mul2(d0, d0), q1 = mul2(d1, d1);
+                    // acc starts at +0: fl(0 + q) = q exactly (q >= +0)
+                    acc0 = x == 0 ? q0 : add2(acc0, q0);
+                    acc1 = x == 0 ? q1 : add2(acc1, q1);
+                }
+                store(la0 + g * lut_stride, acc0, acc1);
             }
-            u64 acc0 = 0, acc1 = 0;
-#pragma unroll
-            for (int x = 0; x < SUB_D; ++x) {
-                const u64 rr = pk2(r[x], r[x]);
-                const u64 d0 = sub2(cen[i][0][x], rr), d1 = sub2(cen[i][1][x], rr);
-                const u64 q0 = mul2(d0, d0), q1 = mul2(d1, d1);
-                // acc starts at +0: fl(0 + q) = q exactly (q >= +0)
-                acc0 = x == 0 ? q0 : add2(acc0, q0);
-                acc1 = x == 0 ? q1 : add2(acc1, q1);
-            }
-            store(lb + i * R * N * E, acc0, acc1);
         }
     }
 
@@ -344,6 +421,146 @@ struct WarpTopK {
     }
 };
 
+// ---------------------------------------------------------------- scanners
+// One LUT gather + widen.  fp8 with N >= 16: the LUT base is 256-byte aligned,
+// so PRMT builds the address (base | code) in one instruction and the row
+// offset b*N rides in the LDS immediate.
+template <int DT, int LOGN, int B>
+__device__ __forceinline__ float ws_gather(uint32_t word, uint32_t base) {
+    constexpr int N = 1 << LOGN;
+    constexpr int OFF = (B << LOGN) * (int)sizeof(typename LutTraits<DT>::T);
+    if constexpr (DT == LUT_E5M3 || DT == LUT_E4M4) {
+        uint32_t v;
+        if constexpr (N >= 16) {
+            const uint32_t addr = __byte_perm(word, base, 0x7650u | (B & 3));
+            asm volatile("ld.shared.u8 %0, [%1+%2];" : "=r"(v) : "r"(addr), "n"(OFF));
+        } else {
+            const uint32_t addr = base + __byte_perm(word, 0u, 0x4440u | (B & 3));
+            asm volatile("ld.shared.u8 %0, [%1+%2];" : "=r"(v) : "r"(addr), "n"(OFF));
+        }
+        return __uint_as_float(v << (23 - LutTraits<DT>::m));
+    } else if constexpr (DT == LUT_F16) {
+        const uint32_t addr = base + (__byte_perm(word, 0u, 0x4440u | (B & 3)) << 1);
+        unsigned short h;
+        asm volatile("ld.shared.u16 %0, [%1+%2];" : "=h"(h) : "r"(addr), "n"(OFF));
+        return __half2float(__ushort_as_half(h));
+    } else {
+        const uint32_t addr = base + (__byte_perm(word, 0u, 0x4440u | (B & 3)) << 2);
+        float v;
+        asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(v) : "r"(addr), "n"(OFF));
+        return v;
+    }
+}
+
+template <int DT, int LOGN, int B>
+__device__ __forceinline__ float ws_acc1(float acc, uint4 w, uint32_t base, int nvalid, bool full) {
+    const uint32_t word = B < 4 ? w.x : B < 8 ? w.y : B < 12 ? w.z : w.w;
+    if (full || B < nvalid) acc = __fadd_rn(acc, ws_gather<DT, LOGN, B>(word, base));
+    return acc;
+}
+
+template <int DT, int LOGN>
+__device__ __forceinline__ float ws_acc16(float acc, uint4 w, uint32_t base, int nvalid, bool full) {
+    acc = ws_acc1<DT, LOGN, 0>(acc, w, base, nvalid, full);
+    acc = ws_acc1<DT, LOGN, 1>(acc, w, base, nvalid, full);
+    acc = ws_acc1<DT, LOGN, 2>(acc, w, base, nvalid, full);
+    acc = ws_acc1<DT, LOGN, 3>(acc, w, base, nvalid, full);
+    acc = ws_acc1<DT, LOGN, 4>(acc, w, base, nvalid, full);
+    acc = ws_acc1<DT, LOGN, 5>(acc, w, base, nvalid, full);
+    acc = ws_acc1<DT, LOGN, 6>(acc, w, base, nvalid, full);
+    acc = ws_acc1<DT, LOGN, 7>(acc, w, base, nvalid, full);
+    acc = ws_acc1<DT, LOGN, 8>(acc, w, base, nvalid, full);
+    acc = ws_acc1<DT, LOGN, 9>(acc, w, base, nvalid, full);
+    acc = ws_acc1<DT, LOGN, 10>(acc, w, base, nvalid, full);
+    acc = ws_acc1<DT, LOGN, 11>(acc, w, base, nvalid, full);
+    acc = ws_acc1<DT, LOGN, 12>(acc, w, base, nvalid, full);
+    acc = ws_acc1<DT, LOGN, 13>(acc, w, base, nvalid, full);
+    acc = ws_acc1<DT, LOGN, 14>(acc, w, base, nvalid, full);
+    acc = ws_acc1<DT, LOGN, 15>(acc, w, base, nvalid, full);
+    return acc;
+}
+
+// Position of a scanner warp in its job's chunk stream: block b (32 vectors
+// of pair g), chunk c of the vectors.
+struct WsCursor {
+    int b, g, c, nb;
+    long long vo;
+    __device__ __forceinline__ void seek(const WsJob* J, int ng, int nblk) {
+        if (b >= nblk) return;
+        while (g + 1 < ng && b >= J->pref[g + 1]) ++g;
+        const int vstart = (b - J->pref[g]) * 32;
+        nb = min(32, J->len[g] - vstart);
+        vo = J->off[g] + vstart;
+    }
+};
+
+// Scan this warp's 32-vector blocks of a job (blocks sw, sw+SW, ...):
+// a rolling window of 4 sixteen-byte code chunks per lane is kept in flight
+// (each chunk consumed is replaced by the load of the chunk 4 positions
+// ahead in the warp's stream), R is accumulated sequentially in j, and keys
+// under the query threshold go to the warp's candidate buffer.
+template <int DT, int LOGN>
+__device__ __forceinline__ void ws_scan_job(const ScanArgs& a, const WsJob* J, int nblk, int ng, int sw, int lane,
+                                            uint32_t lut_s, uint32_t lut_each, WsQuery* S, u64* qlist, int K,
+                                            WarpTopK& tk) {
+    constexpr int N = 1 << LOGN;
+    constexpr int E = (int)sizeof(typename LutTraits<DT>::T);
+    const int nch = a.s_pad >> 4, nfull = a.s >> 4;
+    WsCursor ld{sw, 0, 0, 0, 0}, cs{sw, 0, 0, 0, 0};
+    ld.seek(J, ng, nblk);
+    cs.seek(J, ng, nblk);
+    auto next = [&]() -> uint4 {
+        uint4 r = make_uint4(0, 0, 0, 0);
+        if (ld.b < nblk) {
+            if (lane < ld.nb)
+                r = ld_stream16(a.codes + (size_t)ld.vo * a.s_pad + (size_t)ld.c * ld.nb * 16 + lane * 16);
+            if (++ld.c == nch) {
+                ld.c = 0;
+                ld.b += WS_SW;
+                ld.seek(J, ng, nblk);
+            }
+        }
+        return r;
+    };
+    uint4 w0 = next(), w1 = next(), w2 = next(), w3 = next();
+    float acc = 0.f;
+    uint32_t base = lut_s + cs.g * lut_each;
+    while (cs.b < nblk) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            if (cs.b >= nblk) break;
+            uint4 w;
+            if (i == 0) { w = w0; w0 = next(); }
+            if (i == 1) { w = w1; w1 = next(); }
+            if (i == 2) { w = w2; w2 = next(); }
+            if (i == 3) { w = w3; w3 = next(); }
+            const uint32_t cb = base + (uint32_t)(cs.c * 16 * N * E);
+            if (cs.c < nfull) acc = ws_acc16<DT, LOGN>(acc, w, cb, 16, true);
+            else acc = ws_acc16<DT, LOGN>(acc, w, cb, a.s - 16 * cs.c, false);
+            if (++cs.c == nch) {
+                // vector done
+                u64 key = ~0ull;
+                bool pass = false;
+                if (lane < cs.nb) {
+                    const uint32_t rb = __float_as_uint(lut_finish<DT>(acc));
+                    const u64 tau = *(volatile u64*)&S->tau;
+                    if (rb <= (uint32_t)(tau >> 32)) {
+                        key = ((u64)rb << 32) | a.ids[cs.vo + lane];
+                        pass = key < tau;
+                    }
+                }
+                tk.offer(key, pass);
+                if (tk.n > WS_WBUF - 32) tk.flush(S, qlist, K);
+                acc = 0.f;
+                cs.c = 0;
+                cs.b += WS_SW;
+                cs.seek(J, ng, nblk);
+                base = lut_s + cs.g * lut_each;
+            }
+        }
+    }
+}
+
 // Prep warp: one job = up to G pending probes of query q (pq[from .. from+ng))
 // written into prep-ring entry job % PD (descriptor + padded residuals).
 __device__ __forceinline__ void ws_emit_job(const ScanArgs& a, WsJob* pjobs, float* prq, u64* pfull, u64* pempty,
@@ -382,13 +599,14 @@ __device__ __forceinline__ void ws_emit_job(const ScanArgs& a, WsJob* pjobs, flo
 template <int DT, int LOGN, int SUB_D>
 __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) {
     using T = typename LutTraits<DT>::T;
-    extern __shared__ __align__(16) uint8_t smem[];
+    extern __shared__ __align__(1024) uint8_t ws_smem[];
+    uint8_t* smem = ws_smem;
     const ScanArgs& a = w.a;
     const int G = a.G, NBUF = w.NBUF, K = a.K, NQS = NBUF + 1;
     const WsLayout L(a.d, a.s, SUB_D, LOGN, (int)sizeof(T), G, NBUF, K);
     const size_t lut_each = L.lut_each;
     const int d_pad = (int)L.d_pad;
-    const int jpt = (a.s + WsBuild<DT, LOGN, SUB_D>::R - 1) / WsBuild<DT, LOGN, SUB_D>::R;
+    const int jpt = (a.s + WsBuild<DT, LOGN, SUB_D>::R - 1) / WsBuild<DT, LOGN, SUB_D>::R;  // rows per builder
     u64* pfull = reinterpret_cast<u64*>(smem + L.bars);  // pfull[PD]: job + residuals prepared
     u64* pempty = pfull + WS_PD;                          // pempty[PD]: prep entry consumed
     u64* full = pempty + WS_PD;                           // full[NBUF]: LUTs ready
@@ -401,6 +619,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
     uint8_t* lut_all = smem + L.lut;
     WsPrepQ* pq = reinterpret_cast<WsPrepQ*>(smem + L.prepq);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if ((smem_addr(lut_all) & 255u) != 0u) __trap();  // PRMT LUT addressing needs 256-byte alignment
 
     // ---- setup
     for (int i = threadIdx.x; i < NQS * 2 * K; i += blockDim.x) lists[i] = ~0ull;
@@ -413,6 +632,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
         S->cur = 0;
         S->q = -1;
     }
+    using Builder = WsBuild<DT, LOGN, SUB_D>;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.tmem);
+    if (warp == 0) tmem_alloc<Builder::NCOL>(smem_addr(tmem_slot));
     if (threadIdx.x == 0) {
         for (int b = 0; b < WS_PD; ++b) {
             mbar_init(pfull + b, 1);
@@ -424,9 +646,11 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    tmem_fence_before();
     __syncthreads();
+    tmem_fence_after();
+    const uint32_t tmem = *tmem_slot;
 
-    if (warp >= WS_BW) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(WS_REG_S));
     if (warp == WS_PREP_WARP) {
         // ============================ prep warp ============================
         // Hands out queries, resolves probe keys to (local list, offset,
@@ -514,10 +738,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
         }
     } else if (warp < WS_BW) {
         // =========================== builders ===========================
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(WS_REG_B));
         const int t = threadIdx.x;
-        WsBuild<DT, LOGN, SUB_D> B;
-        B.load(a.centers, a.s, t);
+        Builder B;
+        B.init(a.centers, a.s, t, tmem);
         const uint32_t prq_s = smem_addr(prq), lut_s = smem_addr(lut_all);
         for (int job = 0;; ++job) {
             const int ps = job % WS_PD, slot = job % NBUF;
@@ -533,12 +756,13 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
                 mbar_arrive(full + slot);
                 break;
             }
-            const int ng = PJ->ng;
-            for (int g = 0; g < ng; ++g)
-                B.build(prq_s + (uint32_t)((ps * G + g) * d_pad * 4), lut_s + (uint32_t)((slot * G + g) * lut_each), jpt);
+            B.build(prq_s + (uint32_t)(ps * G * d_pad * 4), (uint32_t)(d_pad * 4), lut_s + (uint32_t)(slot * G * lut_each),
+                    (uint32_t)lut_each, PJ->ng, jpt);
             mbar_arrive(pempty + ps);
             mbar_arrive(full + slot);
         }
+        bar_builders();  // every builder is done with TMEM
+        if (warp == 0) tmem_dealloc<Builder::NCOL>(tmem);
     } else {
         // =========================== scanners ===========================
         const int sw = warp - WS_BW;
@@ -554,28 +778,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
             u64* qlist = lists + (size_t)qs * 2 * K;
             const int ng = J->ng, nblk = J->nblk;
             const uint8_t* lutb = lut_all + (size_t)slot * G * lut_each;  // rows padded; scan reads j < s
-            for (int b = sw; b < nblk; b += WS_SW) {
-                int g = 0;
-                while (g + 1 < ng && b >= J->pref[g + 1]) ++g;
-                const int vstart = (b - J->pref[g]) * 32;
-                const int len = J->len[g];
-                const int nb = min(32, len - vstart);
-                const long long vo = J->off[g] + vstart;
-                u64 key = ~0ull;
-                bool pass = false;
-                if (lane < nb) {
-                    const uint8_t* vb = a.codes + (size_t)vo * a.s_pad + lane * 16;
-                    const float R = scan_vector<DT, LOGN>(vb, nb, reinterpret_cast<const T*>(lutb + g * lut_each), a.s);
-                    const uint32_t rb = __float_as_uint(R);
-                    const u64 tau = *(volatile u64*)&S->tau;
-                    if (rb <= (uint32_t)(tau >> 32)) {
-                        key = ((u64)rb << 32) | a.ids[vo + lane];
-                        pass = key < tau;
-                    }
-                }
-                tk.offer(key, pass);
-                if (tk.n > WS_WBUF - 32) tk.flush(S, qlist, K);
-            }
+            ws_scan_job<DT, LOGN>(a, J, nblk, ng, sw, lane, smem_addr(lutb), (uint32_t)lut_each, S, qlist, K, tk);
             if (J->last) {
                 if (tk.n > 0) tk.flush(S, qlist, K);
                 int d = 0;
