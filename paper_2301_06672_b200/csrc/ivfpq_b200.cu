@@ -360,7 +360,7 @@ int run_select(ivfpq_index* idx, const float* d_q, int64_t nq, int64_t P, uint64
 }
 
 struct WsPlan {
-    int G, NBUF;
+    int G, NBUF, SD;
     size_t smem;
 };
 
@@ -388,18 +388,19 @@ bool ws_plan(const ivfpq_index* idx, int64_t P, int64_t K, int dt, WsPlan* plan)
     const int64_t jpt = 32 / idx->sub_d;
     if ((idx->s + R - 1) / R > jpt) return false;
     const size_t lut_each = WsLayout((int)idx->d, (int)idx->s, (int)idx->sub_d, (int)idx->p, lut_bytes_of((int)dt), 1,
-                                     2, (int)K).lut_each;
+                                     2, (int)K, 2, (int)idx->s_pad).lut_each;
     int G = (int)std::max<size_t>(1, std::min<size_t>(WS_MAX_G, lut_budget_bytes() / lut_each));
     G = (int)std::min<int64_t>(G, std::max<int64_t>(1, P));
     for (; G >= 1; --G)
-        for (int nb = WS_MAX_NBUF; nb >= 2; --nb) {
-            const size_t sm = WsLayout((int)idx->d, (int)idx->s, (int)idx->sub_d, (int)idx->p, lut_bytes_of((int)dt), G,
-                                       nb, (int)K).total;
-            if (sm <= SMEM_LIMIT) {
-                *plan = WsPlan{G, nb, sm};
-                return true;
+        for (int sd = WS_MAX_SD; sd >= 2; --sd)
+            for (int nb = WS_MAX_NBUF; nb >= 2; --nb) {
+                const size_t sm = WsLayout((int)idx->d, (int)idx->s, (int)idx->sub_d, (int)idx->p, lut_bytes_of((int)dt),
+                                           G, nb, (int)K, sd, (int)idx->s_pad).total;
+                if (sm <= SMEM_LIMIT) {
+                    *plan = WsPlan{G, nb, sd, sm};
+                    return true;
+                }
             }
-        }
     return false;
 }
 
@@ -449,6 +450,7 @@ int run_scan(ivfpq_index* idx, const float* d_q, int64_t nq, const uint64_t* d_p
         WsArgs w;
         w.a = a;
         w.NBUF = plan.NBUF;
+        w.SD = plan.SD;
         CKR(idx->work.ensure(16));
         w.work = idx->work.as<int>();
         CK(cudaMemsetAsync(w.work, 0, sizeof(int), st));

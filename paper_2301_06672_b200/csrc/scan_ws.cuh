@@ -46,6 +46,7 @@ constexpr int WS_THREADS = (WS_BW + WS_SW + 1) * 32;
 constexpr int WS_MAX_G = 8;
 constexpr int WS_MAX_NBUF = 3;
 constexpr int WS_PD = 8;                     // prep ring depth (jobs prepared ahead)
+constexpr int WS_MAX_SD = 3;                 // code-block stages per scanner warp
 constexpr int WS_WBUF = 64;                  // per-warp candidate buffer
 constexpr int WS_MAX_K = 512;
 constexpr int WS_BAR_BUILD = 1;              // named barrier id for builders
@@ -54,6 +55,7 @@ constexpr int WS_BAR_BUILD = 1;              // named barrier id for builders
 struct WsArgs {
     ScanArgs a;            // inputs/outputs shared with the v1 kernel
     int NBUF;
+    int SD;                // code-block stages per scanner warp (2..WS_MAX_SD)
     int* work;             // global query counter (zeroed before launch)
 };
 
@@ -124,6 +126,7 @@ __device__ __forceinline__ uint32_t cvt_f16x2_sat(float lo, float hi) {
     return r;
 }
 
+__device__ __forceinline__ uint32_t smem_addr_(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(u64* bar, int count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)), "r"(count));
 }
@@ -141,6 +144,30 @@ __device__ __forceinline__ void mbar_wait(u64* bar, uint32_t parity) {
         "@!p bra WAIT_%=;\n\t}" ::"r"(a),
         "r"(parity)
         : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(u64* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr_(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool mbar_test(u64* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_addr_(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+// TMA bulk copy global -> this CTA's shared memory, completing on `bar`.
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, u64* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(smem_addr_(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+    uint4 r;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(a));
+    return r;
 }
 __device__ __forceinline__ void bar_builders() { asm volatile("bar.sync %0, %1;" ::"n"(WS_BAR_BUILD), "n"(WS_NB) : "memory"); }
 __device__ __forceinline__ float lds_f32(uint32_t a) {
@@ -221,13 +248,14 @@ __device__ __forceinline__ void tmem_st(uint32_t taddr, const uint32_t (&r)[X]) 
 struct WsLayout {
     // lut rows are padded to R * jpt (jpt = ceil(s / R)) so every builder
     // thread runs the same number of rows; rq vectors likewise to R*jpt*sub_d.
-    size_t bars, tmem, jobs, pjobs, prepq, qst, lists, wbuf, prq, lut, total, lut_each, d_pad;
-    __host__ __device__ WsLayout(int d, int s, int sub_d, int logn, int esize, int G, int NBUF, int K) {
+    size_t bars, sbars, tmem, jobs, pjobs, prepq, qst, lists, wbuf, prq, stage, stage_bytes, lut, total, lut_each, d_pad;
+    __host__ __device__ WsLayout(int d, int s, int sub_d, int logn, int esize, int G, int NBUF, int K, int SD, int s_pad) {
         const int N = 1 << logn, R = 1024 / N, jpt = (s + R - 1) / R;
         lut_each = (((size_t)R * jpt * N * esize) + 255) & ~(size_t)255;  // 256-aligned (PRMT addressing)
         d_pad = (size_t)R * jpt * sub_d;
         bars = 0;                                                         // pfull/pempty[PD], full/empty[MAX_NBUF]
-        tmem = (2 * WS_PD + 2 * WS_MAX_NBUF) * 8;                        // u32: TMEM base address
+        sbars = (2 * WS_PD + 2 * WS_MAX_NBUF) * 8;                       // stage barriers [SW][MAX_SD]
+        tmem = sbars + WS_SW * WS_MAX_SD * 8;                             // u32: TMEM base address
         jobs = tmem + 16;                                                 // WsJob[MAX_NBUF] (LUT slots)
         pjobs = jobs + WS_MAX_NBUF * sizeof(WsJob);                       // WsJob[PD] (prep ring)
         prepq = pjobs + WS_PD * sizeof(WsJob);
@@ -238,7 +266,10 @@ struct WsLayout {
         lists = (lists + 15) & ~(size_t)15;
         wbuf = lists + (size_t)(NBUF + 1) * 2 * K * 8;                    // u64[SW][2][WBUF]
         prq = wbuf + (size_t)WS_SW * 2 * WS_WBUF * 8;                     // f32[PD][G][d_pad]
-        lut = prq + (size_t)WS_PD * G * d_pad * 4;                        // [NBUF][G][lut_each]
+        stage = prq + (size_t)WS_PD * G * d_pad * 4;                      // u8[SW][SD][32 * s_pad]
+        stage = (stage + 127) & ~(size_t)127;
+        stage_bytes = (size_t)32 * s_pad;
+        lut = stage + (size_t)WS_SW * SD * stage_bytes;                   // [NBUF][G][lut_each]
         lut = (lut + 255) & ~(size_t)255;
         total = lut + (size_t)NBUF * G * lut_each;
     }
@@ -480,85 +511,114 @@ __device__ __forceinline__ float ws_acc16(float acc, uint4 w, uint32_t base, int
     return acc;
 }
 
-// Position of a scanner warp in its job's chunk stream: block b (32 vectors
-// of pair g), chunk c of the vectors.
-struct WsCursor {
-    int b, g, c, nb;
+// Block k of a job for scanner warp sw is job block b = sw + k*SW: pair g
+// (found incrementally), vectors [vstart, vstart+nb) of list J->lc[g].
+struct WsBlk {
+    int g, nb;
     long long vo;
-    __device__ __forceinline__ void seek(const WsJob* J, int ng, int nblk) {
-        if (b >= nblk) return;
-        while (g + 1 < ng && b >= J->pref[g + 1]) ++g;
-        const int vstart = (b - J->pref[g]) * 32;
-        nb = min(32, J->len[g] - vstart);
-        vo = J->off[g] + vstart;
+};
+__device__ __forceinline__ WsBlk ws_blk(const WsJob* J, int ng, int b, int g) {
+    while (g + 1 < ng && b >= J->pref[g + 1]) ++g;
+    const int vstart = (b - J->pref[g]) * 32;
+    return WsBlk{g, min(32, J->len[g] - vstart), J->off[g] + vstart};
+}
+
+// Per-warp ring of SD code-block stages filled by TMA bulk copies.  The
+// producer side (lane 0) runs ahead of the consumer across job boundaries:
+// the next job's descriptor is used as soon as its LUT-ready barrier has
+// completed (non-blocking test), never more than NBUF-1 jobs ahead, so the
+// slot it reads cannot have been recycled.
+struct WsStager {
+    uint32_t stage0;      // smem address of this warp's stage 0
+    uint32_t stage_bytes;
+    u64* sbar;            // this warp's SD stage barriers
+    int SD, NBUF, sw;
+    int issued, consumed; // blocks
+    int pjob, pb, pg;     // producer cursor: job, block index, pair hint
+    bool pready, pend;
+    const WsJob* PJ;
+
+    __device__ __forceinline__ void top_up(const ScanArgs& a, const WsJob* jobs, u64* full, int cjob, int lane) {
+        while (issued - consumed < SD && !pend) {
+            if (!pready) {
+                if (pjob >= cjob + NBUF) return;
+                const int slot = pjob % NBUF;
+                if (pjob != cjob && !mbar_test(full + slot, (pjob / NBUF) & 1)) return;
+                PJ = jobs + slot;
+                pready = true;
+                pb = sw;
+                pg = 0;
+                if (PJ->qs < 0) {
+                    pend = true;
+                    return;
+                }
+            }
+            if (pb >= PJ->nblk) {
+                ++pjob;
+                pready = false;
+                continue;
+            }
+            const WsBlk k = ws_blk(PJ, PJ->ng, pb, pg);
+            pg = k.g;
+            if (lane == 0) {
+                const int st = issued % SD;
+                const uint32_t bytes = (uint32_t)k.nb * (uint32_t)a.s_pad;
+                fence_proxy_async();  // earlier generic reads of this stage before the async overwrite
+                mbar_expect_tx(sbar + st, bytes);
+                bulk_g2s(stage0 + st * stage_bytes, a.codes + (size_t)k.vo * a.s_pad, bytes, sbar + st);
+            }
+            ++issued;
+            pb += WS_SW;
+        }
     }
 };
 
-// Scan this warp's 32-vector blocks of a job (blocks sw, sw+SW, ...):
-// a rolling window of 4 sixteen-byte code chunks per lane is kept in flight
-// (each chunk consumed is replaced by the load of the chunk 4 positions
-// ahead in the warp's stream), R is accumulated sequentially in j, and keys
-// under the query threshold go to the warp's candidate buffer.
+// Scan one job's blocks for this warp from the stage ring: R accumulated
+// sequentially in j from LUT gathers; keys under the query threshold go to
+// the warp's candidate buffer.
 template <int DT, int LOGN>
-__device__ __forceinline__ void ws_scan_job(const ScanArgs& a, const WsJob* J, int nblk, int ng, int sw, int lane,
-                                            uint32_t lut_s, uint32_t lut_each, WsQuery* S, u64* qlist, int K,
-                                            WarpTopK& tk) {
+__device__ __forceinline__ void ws_scan_job(const ScanArgs& a, const WsJob* J, const WsJob* jobs, u64* full, int cjob,
+                                            int sw, int lane, uint32_t lut_s, uint32_t lut_each, WsQuery* S,
+                                            u64* qlist, int K, WarpTopK& tk, WsStager& sg) {
     constexpr int N = 1 << LOGN;
     constexpr int E = (int)sizeof(typename LutTraits<DT>::T);
-    const int nch = a.s_pad >> 4, nfull = a.s >> 4;
-    WsCursor ld{sw, 0, 0, 0, 0}, cs{sw, 0, 0, 0, 0};
-    ld.seek(J, ng, nblk);
-    cs.seek(J, ng, nblk);
-    auto next = [&]() -> uint4 {
-        uint4 r = make_uint4(0, 0, 0, 0);
-        if (ld.b < nblk) {
-            if (lane < ld.nb)
-                r = ld_stream16(a.codes + (size_t)ld.vo * a.s_pad + (size_t)ld.c * ld.nb * 16 + lane * 16);
-            if (++ld.c == nch) {
-                ld.c = 0;
-                ld.b += WS_SW;
-                ld.seek(J, ng, nblk);
+    const int nch = a.s_pad >> 4, nfull = a.s >> 4, ng = J->ng, nblk = J->nblk;
+    int g = 0;
+    for (int b = sw; b < nblk; b += WS_SW) {
+        sg.top_up(a, jobs, full, cjob, lane);
+        const WsBlk k = ws_blk(J, ng, b, g);
+        g = k.g;
+        const int st = sg.consumed % sg.SD;
+        mbar_wait(sg.sbar + st, (sg.consumed / sg.SD) & 1);
+        const uint32_t src = sg.stage0 + st * sg.stage_bytes + lane * 16, cstride = (uint32_t)k.nb * 16;
+        const uint32_t base = lut_s + k.g * lut_each;
+        float acc = 0.f;
+        int c = 0;
+        for (; c + 2 <= nfull; c += 2) {
+            const uint4 w0 = lds128(src + c * cstride), w1 = lds128(src + (c + 1) * cstride);
+            acc = ws_acc16<DT, LOGN>(acc, w0, base + (uint32_t)(c * 16 * N * E), 16, true);
+            acc = ws_acc16<DT, LOGN>(acc, w1, base + (uint32_t)((c + 1) * 16 * N * E), 16, true);
+        }
+        for (; c < nch; ++c) {
+            const uint4 w0 = lds128(src + c * cstride);
+            acc = ws_acc16<DT, LOGN>(acc, w0, base + (uint32_t)(c * 16 * N * E), a.s - 16 * c, c < nfull);
+        }
+        __syncwarp();
+        ++sg.consumed;
+        u64 key = ~0ull;
+        bool pass = false;
+        if (lane < k.nb) {
+            const uint32_t rb = __float_as_uint(lut_finish<DT>(acc));
+            const u64 tau = *(volatile u64*)&S->tau;
+            if (rb <= (uint32_t)(tau >> 32)) {
+                key = ((u64)rb << 32) | a.ids[k.vo + lane];
+                pass = key < tau;
             }
         }
-        return r;
-    };
-    uint4 w0 = next(), w1 = next(), w2 = next(), w3 = next();
-    float acc = 0.f;
-    uint32_t base = lut_s + cs.g * lut_each;
-    while (cs.b < nblk) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            if (cs.b >= nblk) break;
-            uint4 w;
-            if (i == 0) { w = w0; w0 = next(); }
-            if (i == 1) { w = w1; w1 = next(); }
-            if (i == 2) { w = w2; w2 = next(); }
-            if (i == 3) { w = w3; w3 = next(); }
-            const uint32_t cb = base + (uint32_t)(cs.c * 16 * N * E);
-            if (cs.c < nfull) acc = ws_acc16<DT, LOGN>(acc, w, cb, 16, true);
-            else acc = ws_acc16<DT, LOGN>(acc, w, cb, a.s - 16 * cs.c, false);
-            if (++cs.c == nch) {
-                // vector done
-                u64 key = ~0ull;
-                bool pass = false;
-                if (lane < cs.nb) {
-                    const uint32_t rb = __float_as_uint(lut_finish<DT>(acc));
-                    const u64 tau = *(volatile u64*)&S->tau;
-                    if (rb <= (uint32_t)(tau >> 32)) {
-                        key = ((u64)rb << 32) | a.ids[cs.vo + lane];
-                        pass = key < tau;
-                    }
-                }
-                tk.offer(key, pass);
-                if (tk.n > WS_WBUF - 32) tk.flush(S, qlist, K);
-                acc = 0.f;
-                cs.c = 0;
-                cs.b += WS_SW;
-                cs.seek(J, ng, nblk);
-                base = lut_s + cs.g * lut_each;
-            }
-        }
+        tk.offer(key, pass);
+        if (tk.n > WS_WBUF - 32) tk.flush(S, qlist, K);
     }
+    sg.top_up(a, jobs, full, cjob, lane);  // keep the ring busy into the next job(s)
 }
 
 // Prep warp: one job = up to G pending probes of query q (pq[from .. from+ng))
@@ -603,7 +663,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
     uint8_t* smem = ws_smem;
     const ScanArgs& a = w.a;
     const int G = a.G, NBUF = w.NBUF, K = a.K, NQS = NBUF + 1;
-    const WsLayout L(a.d, a.s, SUB_D, LOGN, (int)sizeof(T), G, NBUF, K);
+    const int SD = w.SD;
+    const WsLayout L(a.d, a.s, SUB_D, LOGN, (int)sizeof(T), G, NBUF, K, SD, a.s_pad);
     const size_t lut_each = L.lut_each;
     const int d_pad = (int)L.d_pad;
     const int jpt = (a.s + WsBuild<DT, LOGN, SUB_D>::R - 1) / WsBuild<DT, LOGN, SUB_D>::R;  // rows per builder
@@ -644,6 +705,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
             mbar_init(full + b, WS_NB);
             mbar_init(empty + b, WS_SW);
         }
+        u64* sb = reinterpret_cast<u64*>(smem + L.sbars);
+        for (int b = 0; b < WS_SW * WS_MAX_SD; ++b) mbar_init(sb + b, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     tmem_fence_before();
@@ -768,6 +831,20 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
         const int sw = warp - WS_BW;
         u64* wb = reinterpret_cast<u64*>(smem + L.wbuf) + (size_t)sw * 2 * WS_WBUF;
         WarpTopK tk{wb, wb + WS_WBUF, 0};
+        WsStager sg;
+        sg.stage0 = smem_addr(smem + L.stage) + (uint32_t)(sw * SD * L.stage_bytes);
+        sg.stage_bytes = (uint32_t)L.stage_bytes;
+        sg.sbar = reinterpret_cast<u64*>(smem + L.sbars) + sw * WS_MAX_SD;
+        sg.SD = SD;
+        sg.NBUF = NBUF;
+        sg.sw = sw;
+        sg.issued = sg.consumed = 0;
+        sg.pjob = 0;
+        sg.pb = sw;
+        sg.pg = 0;
+        sg.pready = false;
+        sg.pend = false;
+        sg.PJ = nullptr;
         for (int job = 0;; ++job) {
             const int slot = job % NBUF;
             mbar_wait(full + slot, (job / NBUF) & 1);
@@ -776,9 +853,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
             if (qs < 0) break;
             WsQuery* S = qst + qs;
             u64* qlist = lists + (size_t)qs * 2 * K;
-            const int ng = J->ng, nblk = J->nblk;
             const uint8_t* lutb = lut_all + (size_t)slot * G * lut_each;  // rows padded; scan reads j < s
-            ws_scan_job<DT, LOGN>(a, J, nblk, ng, sw, lane, smem_addr(lutb), (uint32_t)lut_each, S, qlist, K, tk);
+            ws_scan_job<DT, LOGN>(a, J, jobs, full, job, sw, lane, smem_addr(lutb), (uint32_t)lut_each, S, qlist, K, tk, sg);
             if (J->last) {
                 if (tk.n > 0) tk.flush(S, qlist, K);
                 int d = 0;
