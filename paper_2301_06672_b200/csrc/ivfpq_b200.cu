@@ -66,7 +66,7 @@ constexpr size_t COARSE_CHUNK_BYTES = 256ull << 20;
 size_t lut_budget_bytes() {
     static size_t v = [] {
         const char* e = getenv("IVFPQ_LUT_BUDGET_KB");
-        return (size_t)(e ? atoi(e) : 64) * 1024;
+        return (size_t)(e ? atoi(e) : 32) * 1024;
     }();
     return v;
 }

@@ -44,7 +44,8 @@ constexpr int WS_NB = WS_BW * 32;            // 256 builder threads
 constexpr int WS_PREP_WARP = WS_BW + WS_SW;   // warp 19: job preparation (in the last scanner warpgroup)
 constexpr int WS_THREADS = (WS_BW + WS_SW + 1) * 32;
 constexpr int WS_MAX_G = 8;
-constexpr int WS_MAX_NBUF = 3;
+constexpr int WS_MAX_NBUF = 6;
+constexpr int WS_NQS = 4;                    // per-query states (query top-k lists) in flight
 constexpr int WS_PD = 8;                     // prep ring depth (jobs prepared ahead)
 constexpr int WS_MAX_SD = 3;                 // code-block stages per scanner warp
 constexpr int WS_WBUF = 64;                  // per-warp candidate buffer
@@ -248,23 +249,24 @@ __device__ __forceinline__ void tmem_st(uint32_t taddr, const uint32_t (&r)[X]) 
 struct WsLayout {
     // lut rows are padded to R * jpt (jpt = ceil(s / R)) so every builder
     // thread runs the same number of rows; rq vectors likewise to R*jpt*sub_d.
-    size_t bars, sbars, tmem, jobs, pjobs, prepq, qst, lists, wbuf, prq, stage, stage_bytes, lut, total, lut_each, d_pad;
+    size_t bars, sbars, qfree, tmem, jobs, pjobs, prepq, qst, lists, wbuf, prq, stage, stage_bytes, lut, total, lut_each, d_pad;
     __host__ __device__ WsLayout(int d, int s, int sub_d, int logn, int esize, int G, int NBUF, int K, int SD, int s_pad) {
         const int N = 1 << logn, R = 1024 / N, jpt = (s + R - 1) / R;
         lut_each = (((size_t)R * jpt * N * esize) + 255) & ~(size_t)255;  // 256-aligned (PRMT addressing)
         d_pad = (size_t)R * jpt * sub_d;
         bars = 0;                                                         // pfull/pempty[PD], full/empty[MAX_NBUF]
         sbars = (2 * WS_PD + 2 * WS_MAX_NBUF) * 8;                       // stage barriers [SW][MAX_SD]
-        tmem = sbars + WS_SW * WS_MAX_SD * 8;                             // u32: TMEM base address
+        qfree = sbars + WS_SW * WS_MAX_SD * 8;                            // query-state free barriers [NQS]
+        tmem = qfree + WS_NQS * 8;                                        // u32: TMEM base address
         jobs = tmem + 16;                                                 // WsJob[MAX_NBUF] (LUT slots)
         pjobs = jobs + WS_MAX_NBUF * sizeof(WsJob);                       // WsJob[PD] (prep ring)
         prepq = pjobs + WS_PD * sizeof(WsJob);
         prepq = (prepq + 15) & ~(size_t)15;
-        qst = prepq + sizeof(WsPrepQ);                                    // WsQuery[MAX_NBUF+1]
+        qst = prepq + sizeof(WsPrepQ);                                    // WsQuery[NQS]
         qst = (qst + 15) & ~(size_t)15;
-        lists = qst + (WS_MAX_NBUF + 1) * sizeof(WsQuery);                // u64[NBUF+1][2][K]
+        lists = qst + WS_NQS * sizeof(WsQuery);                           // u64[NQS][2][K]
         lists = (lists + 15) & ~(size_t)15;
-        wbuf = lists + (size_t)(NBUF + 1) * 2 * K * 8;                    // u64[SW][2][WBUF]
+        wbuf = lists + (size_t)WS_NQS * 2 * K * 8;                        // u64[SW][2][WBUF]
         prq = wbuf + (size_t)WS_SW * 2 * WS_WBUF * 8;                     // f32[PD][G][d_pad]
         stage = prq + (size_t)WS_PD * G * d_pad * 4;                      // u8[SW][SD][32 * s_pad]
         stage = (stage + 127) & ~(size_t)127;
@@ -662,7 +664,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
     extern __shared__ __align__(1024) uint8_t ws_smem[];
     uint8_t* smem = ws_smem;
     const ScanArgs& a = w.a;
-    const int G = a.G, NBUF = w.NBUF, K = a.K, NQS = NBUF + 1;
+    const int G = a.G, NBUF = w.NBUF, K = a.K, NQS = WS_NQS;
     const int SD = w.SD;
     const WsLayout L(a.d, a.s, SUB_D, LOGN, (int)sizeof(T), G, NBUF, K, SD, a.s_pad);
     const size_t lut_each = L.lut_each;
@@ -684,7 +686,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
 
     // ---- setup
     for (int i = threadIdx.x; i < NQS * 2 * K; i += blockDim.x) lists[i] = ~0ull;
-    if (threadIdx.x < NQS) {
+    if (threadIdx.x < WS_NQS) {
         WsQuery* S = qst + threadIdx.x;
         S->tau = ~0ull;
         S->ncand = 0;
@@ -707,6 +709,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
         }
         u64* sb = reinterpret_cast<u64*>(smem + L.sbars);
         for (int b = 0; b < WS_SW * WS_MAX_SD; ++b) mbar_init(sb + b, 1);
+        u64* qf = reinterpret_cast<u64*>(smem + L.qfree);
+        for (int b = 0; b < WS_NQS; ++b) mbar_init(qf + b, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     tmem_fence_before();
@@ -736,6 +740,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
             ++qseq;
             const int qs = qseq % NQS;
             WsQuery* S = qst + qs;
+            // the state is reused only after the query that last held it was finalised
+            if (qseq >= NQS) mbar_wait(reinterpret_cast<u64*>(smem + L.qfree) + qs, ((qseq / NQS) - 1) & 1);
             if (lane == 0) {
                 S->q = q;
                 S->ncand = 0;
@@ -883,12 +889,13 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
                     }
                     __syncwarp();
                     for (int i = lane; i < 2 * K; i += 32) qlist[i] = ~0ull;
+                    __syncwarp();
                     if (lane == 0) {
                         S->tau = ~0ull;
                         S->cur = 0;
                         S->done = 0;
+                        mbar_arrive(reinterpret_cast<u64*>(smem + L.qfree) + qs);  // release: state free
                     }
-                    __threadfence_block();
                 }
             }
             __syncwarp();

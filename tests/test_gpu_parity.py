@@ -296,3 +296,21 @@ def test_device_search_on_side_stream(pkg):
         pkg.search_device(dev, q, params, oi, od, osh)
         got = oi.cpu().numpy()
     assert np.array_equal(got, c["ids_f16_k10_p8"])
+
+
+@pytest.mark.parametrize("nprobe,k", [(1, 10), (2, 5), (3, 100)])
+def test_many_short_queries_reuse_query_state(pkg, nprobe, k):
+    """Thousands of queries with 1-3 probed lists each: every persistent CTA
+    cycles through many queries, exercising the per-query state ring."""
+    from oracle import c_oracle
+    rng = np.random.default_rng(nprobe)
+    idx = _random_index(rng, 40000, 64, 32, 8, 256)
+    q = rng.random((6000, 64)).astype(np.float32)
+    off, ids, codes = idx.csr()
+    for prec in ("f32", "e5m3"):
+        got, n_short = pkg.search_batch(idx, q, pkg.SearchParams(k=k, nprobe=nprobe, precision=prec))
+        want_ids, want_d, want_short = c_oracle.search_batch(idx.coarse, idx.cb.centers, off, ids, codes, q, k,
+                                                             nprobe, prec)
+        assert np.array_equal(got.ids, want_ids), prec
+        assert np.array_equal(got.distances, want_d), prec
+        assert n_short == want_short
