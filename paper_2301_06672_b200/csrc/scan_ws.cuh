@@ -536,7 +536,9 @@ struct WsStager {
     u64* sbar;            // this warp's SD stage barriers
     int SD, NBUF, sw;
     int issued, consumed; // blocks
+    int ps, cs, cph;      // producer stage, consumer stage, consumer phase (no runtime div/mod)
     int pjob, pb, pg;     // producer cursor: job, block index, pair hint
+    int pslot, pph;       // LUT slot of pjob and its full-barrier phase
     bool pready, pend;
     const WsJob* PJ;
 
@@ -544,9 +546,8 @@ struct WsStager {
         while (issued - consumed < SD && !pend) {
             if (!pready) {
                 if (pjob >= cjob + NBUF) return;
-                const int slot = pjob % NBUF;
-                if (pjob != cjob && !mbar_test(full + slot, (pjob / NBUF) & 1)) return;
-                PJ = jobs + slot;
+                if (pjob != cjob && !mbar_test(full + pslot, pph)) return;
+                PJ = jobs + pslot;
                 pready = true;
                 pb = sw;
                 pg = 0;
@@ -557,19 +558,24 @@ struct WsStager {
             }
             if (pb >= PJ->nblk) {
                 ++pjob;
+                if (++pslot == NBUF) {
+                    pslot = 0;
+                    pph ^= 1;
+                }
                 pready = false;
                 continue;
             }
             const WsBlk k = ws_blk(PJ, PJ->ng, pb, pg);
             pg = k.g;
             if (lane == 0) {
-                const int st = issued % SD;
+                const int st = ps;
                 const uint32_t bytes = (uint32_t)k.nb * (uint32_t)a.s_pad;
                 fence_proxy_async();  // earlier generic reads of this stage before the async overwrite
                 mbar_expect_tx(sbar + st, bytes);
                 bulk_g2s(stage0 + st * stage_bytes, a.codes + (size_t)k.vo * a.s_pad, bytes, sbar + st);
             }
             ++issued;
+            ps = ps + 1 == SD ? 0 : ps + 1;
             pb += WS_SW;
         }
     }
@@ -590,8 +596,8 @@ __device__ __forceinline__ void ws_scan_job(const ScanArgs& a, const WsJob* J, c
         sg.top_up(a, jobs, full, cjob, lane);
         const WsBlk k = ws_blk(J, ng, b, g);
         g = k.g;
-        const int st = sg.consumed % sg.SD;
-        mbar_wait(sg.sbar + st, (sg.consumed / sg.SD) & 1);
+        const int st = sg.cs;
+        mbar_wait(sg.sbar + st, sg.cph);
         const uint32_t src = sg.stage0 + st * sg.stage_bytes + lane * 16, cstride = (uint32_t)k.nb * 16;
         const uint32_t base = lut_s + k.g * lut_each;
         float acc = 0.f;
@@ -607,6 +613,10 @@ __device__ __forceinline__ void ws_scan_job(const ScanArgs& a, const WsJob* J, c
         }
         __syncwarp();
         ++sg.consumed;
+        if (++sg.cs == sg.SD) {
+            sg.cs = 0;
+            sg.cph ^= 1;
+        }
         u64 key = ~0ull;
         bool pass = false;
         if (lane < k.nb) {
@@ -811,10 +821,12 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
         Builder B;
         B.init(a.centers, a.s, t, tmem);
         const uint32_t prq_s = smem_addr(prq), lut_s = smem_addr(lut_all);
+        int slot = 0, eph = 0;  // LUT slot of this job, parity of its previous release
+        bool wrapped = false;
         for (int job = 0;; ++job) {
-            const int ps = job % WS_PD, slot = job % NBUF;
+            const int ps = job % WS_PD;
             mbar_wait(pfull + ps, (job / WS_PD) & 1);
-            if (job >= NBUF) mbar_wait(empty + slot, ((job / NBUF) - 1) & 1);
+            if (wrapped) mbar_wait(empty + slot, eph);
             const WsJob* PJ = pjobs + ps;
             if (t < 32) {  // the descriptor travels with the LUT slot (warp 0 copies it)
                 const int* src = reinterpret_cast<const int*>(PJ);
@@ -829,6 +841,11 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
                     (uint32_t)lut_each, PJ->ng, jpt);
             mbar_arrive(pempty + ps);
             mbar_arrive(full + slot);
+            if (++slot == NBUF) {
+                slot = 0;
+                if (wrapped) eph ^= 1;
+                wrapped = true;
+            }
         }
         bar_builders();  // every builder is done with TMEM
         if (warp == 0) tmem_dealloc<Builder::NCOL>(tmem);
@@ -845,15 +862,17 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
         sg.NBUF = NBUF;
         sg.sw = sw;
         sg.issued = sg.consumed = 0;
+        sg.ps = sg.cs = sg.cph = 0;
+        sg.pslot = sg.pph = 0;
         sg.pjob = 0;
         sg.pb = sw;
         sg.pg = 0;
         sg.pready = false;
         sg.pend = false;
         sg.PJ = nullptr;
+        int slot = 0, fph = 0;
         for (int job = 0;; ++job) {
-            const int slot = job % NBUF;
-            mbar_wait(full + slot, (job / NBUF) & 1);
+            mbar_wait(full + slot, fph);
             const WsJob* J = jobs + slot;
             const int qs = J->qs;
             if (qs < 0) break;
@@ -900,6 +919,10 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(empty + slot);
+            if (++slot == NBUF) {
+                slot = 0;
+                fph ^= 1;
+            }
         }
     }
 }
