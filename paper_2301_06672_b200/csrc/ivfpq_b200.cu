@@ -384,8 +384,8 @@ bool ws_plan(const ivfpq_index* idx, int64_t P, int64_t K, int dt, WsPlan* plan)
     if (ws_disabled() || idx->num_sms <= 0) return false;
     const int64_t N = 1LL << idx->p;
     if (idx->p < 2 || idx->sub_d < 1 || idx->sub_d > 4 || K > WS_MAX_K) return false;
-    const int64_t R = 1024 / N;
-    const int64_t jpt = 32 / idx->sub_d;
+    const int64_t R = WS_R((int)N);
+    const int64_t jpt = WS_JPT((int)idx->sub_d);
     if ((idx->s + R - 1) / R > jpt) return false;
     const size_t lut_each = WsLayout((int)idx->d, (int)idx->s, (int)idx->sub_d, (int)idx->p, lut_bytes_of((int)dt), 1,
                                      2, (int)K, 2, (int)idx->s_pad).lut_each;

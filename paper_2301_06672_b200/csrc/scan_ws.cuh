@@ -5,7 +5,7 @@
 //
 //  * one CTA per SM (persistent), queries handed out by a global atomic;
 //  * the whole PQ codebook lives in TENSOR MEMORY (128 KiB of the SM's 256 KiB
-//    TMEM, tcgen05.alloc/st/ld): 8 BUILDER warps each read only their own
+//    TMEM, tcgen05.alloc/st/ld): 16 BUILDER warps each read only their own
 //    lane's columns: builder thread t owns a quad of codes m = 4u..4u+3 and
 //    the subspaces j = jr, jr+R, ... (u = t % (N/4), jr = t / (N/4),
 //    R = 1024/N); one tcgen05.ld of a row's centers serves all G lists of a
@@ -16,7 +16,7 @@
 //           min_normal become subnormal and flush to +0), then the code is
 //           min(bits >> (23-m), 255), done two-at-a-time with u16x2 min.
 //      f16: cvt.rn.satfinite.f16x2.f32 (= RNE of min(x, 65504)).
-//  * 11 SCANNER warps stream 32-vector code
+//  * 15 SCANNER warps stream 32-vector code
 //    blocks (16-byte non-allocating loads, interleaved layout) and look the
 //    codes up in the slot's LUTs; R accumulates sequentially in j (fp32).
 //  * one PREP warp hands out queries, resolves probe keys 32 at a time and
@@ -38,10 +38,14 @@
 
 namespace ivfpq {
 
-constexpr int WS_BW = 8;                     // builder warps
-constexpr int WS_SW = 11;                    // scanner warps (+1 prep warp = 3 warpgroups)
-constexpr int WS_NB = WS_BW * 32;            // 256 builder threads
-constexpr int WS_PREP_WARP = WS_BW + WS_SW;   // warp 19: job preparation (in the last scanner warpgroup)
+constexpr int WS_BW = 16;                    // builder warps (4 TMEM column groups)
+constexpr int WS_SW = 15;                    // scanner warps
+constexpr int WS_NB = WS_BW * 32;            // 512 builder threads
+constexpr int WS_PREP_WARP = WS_BW + WS_SW;   // warp 31: job preparation
+// Builder row geometry (shared by host plan and device): a builder thread owns
+// a quad of codes and ceil(s / WS_R(N)) subspace rows, at most WS_JPT(sub_d).
+__host__ __device__ constexpr int WS_R(int N) { return WS_NB * 4 / N; }
+__host__ __device__ constexpr int WS_JPT(int sub_d) { return 64 / (sub_d * WS_BW / 4); }
 constexpr int WS_THREADS = (WS_BW + WS_SW + 1) * 32;
 constexpr int WS_MAX_G = 8;
 constexpr int WS_MAX_NBUF = 6;
@@ -251,7 +255,7 @@ struct WsLayout {
     // thread runs the same number of rows; rq vectors likewise to R*jpt*sub_d.
     size_t bars, sbars, qfree, tmem, jobs, pjobs, prepq, qst, lists, wbuf, prq, stage, stage_bytes, lut, total, lut_each, d_pad;
     __host__ __device__ WsLayout(int d, int s, int sub_d, int logn, int esize, int G, int NBUF, int K, int SD, int s_pad) {
-        const int N = 1 << logn, R = 1024 / N, jpt = (s + R - 1) / R;
+        const int N = 1 << logn, R = WS_R(N), jpt = (s + R - 1) / R;
         lut_each = (((size_t)R * jpt * N * esize) + 255) & ~(size_t)255;  // 256-aligned (PRMT addressing)
         d_pad = (size_t)R * jpt * sub_d;
         bars = 0;                                                         // pfull/pempty[PD], full/empty[MAX_NBUF]
@@ -286,11 +290,13 @@ template <int DT, int LOGN, int SUB_D>
 struct WsBuild {
     static constexpr int N = 1 << LOGN;
     static constexpr int NQ4 = N / 4;                                   // quads per subspace row
-    static constexpr int R = WS_NB / NQ4;                               // row groups
-    static constexpr int JPT = 32 / SUB_D;                              // max owned rows (host-checked)
+    static constexpr int R = WS_R(N);                                   // row groups
+    static constexpr int JPT = WS_JPT(SUB_D);                           // max owned rows (host-checked)
     static constexpr int CPI = SUB_D == 1 ? 4 : SUB_D == 2 ? 8 : 16;    // TMEM columns per owned row
-    static constexpr int HALF = JPT * CPI;                              // columns per builder half
-    static constexpr int NCOL = 2 * HALF <= 256 ? 256 : 512;            // TMEM allocation
+    static constexpr int HALF = JPT * CPI;                              // columns per builder column group
+    static constexpr int NGRP = WS_BW / 4;                              // warps sharing a TMEM lane quarter
+    static constexpr int NCOL = NGRP * HALF <= 256 ? 256 : 512;         // TMEM allocation
+    static_assert(NGRP * HALF <= 512, "codebook does not fit TMEM");
     using T = typename LutTraits<DT>::T;
 
     int u, jr;
