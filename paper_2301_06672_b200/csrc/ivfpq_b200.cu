@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "../../include/ivfpq_b200.h"
+#define IVFPQ_DEFINE_PLAN_KERNEL
 #include "codec.cuh"
 #include "coarse.cuh"
 #include "scan.cuh"
@@ -112,7 +113,7 @@ struct ivfpq_index {
     cudaStream_t stream = nullptr;
     std::mutex mu;
     // scratch
-    DevBuf q, dist, pkeys, oids, odist, oshort, keys, ncand, work;
+    DevBuf q, dist, pkeys, oids, odist, oshort, keys, ncand, work, plan_jobs, plan_rq, plan_nj, plan_nc;
     int num_sms = 0;
 };
 
@@ -436,6 +437,7 @@ int run_scan(ivfpq_index* idx, const float* d_q, int64_t nq, const uint64_t* d_p
     a.s_pad = (int)idx->s_pad;
     a.K = (int)K;
     a.G = G;
+    a.debug_skip_gather = 0;
     a.out_keys = out_keys;
     a.out_ncand = out_ncand;
     a.out_ids = out_ids;
@@ -451,9 +453,33 @@ int run_scan(ivfpq_index* idx, const float* d_q, int64_t nq, const uint64_t* d_p
         w.a = a;
         w.NBUF = plan.NBUF;
         w.SD = plan.SD;
+        static const int dbg = [] {
+            const char* e = getenv("IVFPQ_WS_DEBUG");
+            return e ? atoi(e) : 0;
+        }();
+        w.debug = dbg;
+        w.a.debug_skip_gather = (dbg & 2) != 0;
         CKR(idx->work.ensure(16));
         w.work = idx->work.as<int>();
         CK(cudaMemsetAsync(w.work, 0, sizeof(int), st));
+        // plan: job descriptors + residual rows per query
+        const WsLayout lay((int)idx->d, (int)idx->s, (int)idx->sub_d, (int)idx->p, lut_bytes_of(dt), plan.G, plan.NBUF,
+                           (int)K, plan.SD, (int)idx->s_pad);
+        const int d_pad = (int)lay.d_pad;
+        const int JMAX = (int)std::max<int64_t>(1, (P + plan.G - 1) / plan.G);
+        CKR(idx->plan_jobs.ensure((size_t)nq * JMAX * sizeof(WsJob)));
+        CKR(idx->plan_rq.ensure((size_t)nq * JMAX * plan.G * d_pad * 4));
+        CKR(idx->plan_nj.ensure((size_t)nq * 4));
+        CKR(idx->plan_nc.ensure((size_t)nq * 8));
+        w.plan_jobs = idx->plan_jobs.as<WsJob>();
+        w.plan_rq = idx->plan_rq.as<float>();
+        w.plan_njobs = idx->plan_nj.as<int>();
+        w.plan_ncand = idx->plan_nc.as<long long>();
+        w.JMAX = JMAX;
+        ws_plan_kernel<<<(unsigned)((nq + 7) / 8), 256, 0, st>>>(a, plan.G, d_pad, JMAX, idx->plan_jobs.as<WsJob>(),
+                                                                   idx->plan_rq.as<float>(), idx->plan_nj.as<int>(),
+                                                                   idx->plan_nc.as<long long>());
+        KCHECK();
         const int grid = std::min<int64_t>(idx->num_sms, nq);
         cudaError_t e = cudaErrorInvalidValue;
         switch (dt) {
@@ -642,7 +668,7 @@ int ivfpq_index_destroy(ivfpq_index* idx) {
     for (void* ptr : ptrs)
         if (ptr) cudaFree(ptr);
     for (DevBuf* b : {&idx->q, &idx->dist, &idx->pkeys, &idx->oids, &idx->odist, &idx->oshort, &idx->keys, &idx->ncand,
-                      &idx->work})
+                      &idx->work, &idx->plan_jobs, &idx->plan_rq, &idx->plan_nj, &idx->plan_nc})
         b->release();
     if (idx->stream) cudaStreamDestroy(idx->stream);
     delete idx;

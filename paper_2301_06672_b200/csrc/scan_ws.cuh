@@ -57,10 +57,18 @@ constexpr int WS_MAX_K = 512;
 constexpr int WS_BAR_BUILD = 1;              // named barrier id for builders
 
 
+struct WsJob;
 struct WsArgs {
     ScanArgs a;            // inputs/outputs shared with the v1 kernel
+    const WsJob* plan_jobs;      // [nq][JMAX] job descriptors (ws_plan_kernel)
+    const float* plan_rq;        // [nq][JMAX][G][d_pad] residuals
+    const int* plan_njobs;       // [nq]
+    const long long* plan_ncand; // [nq]
+    int JMAX;
     int NBUF;
     int SD;                // code-block stages per scanner warp (2..WS_MAX_SD)
+    int debug;             // perf experiments only (wrong results): bit 0 = skip LUT math, bit 1 = skip
+                           // gathers + offers, bit 2 = scanners skip their blocks entirely
     int* work;             // global query counter (zeroed before launch)
 };
 
@@ -263,15 +271,16 @@ struct WsLayout {
         qfree = sbars + WS_SW * WS_MAX_SD * 8;                            // query-state free barriers [NQS]
         tmem = qfree + WS_NQS * 8;                                        // u32: TMEM base address
         jobs = tmem + 16;                                                 // WsJob[MAX_NBUF] (LUT slots)
-        pjobs = jobs + WS_MAX_NBUF * sizeof(WsJob);                       // WsJob[PD] (prep ring)
-        prepq = pjobs + WS_PD * sizeof(WsJob);
-        prepq = (prepq + 15) & ~(size_t)15;
-        qst = prepq + sizeof(WsPrepQ);                                    // WsQuery[NQS]
+        pjobs = jobs + WS_MAX_NBUF * sizeof(WsJob);                       // WsJob[PD] (prep ring, TMA-filled)
+        pjobs = (pjobs + 127) & ~(size_t)127;
+        prepq = pjobs + WS_PD * sizeof(WsJob);                            // int[PD]: query state of each prep entry
+        qst = prepq + WS_PD * 4;                                          // WsQuery[NQS]
         qst = (qst + 15) & ~(size_t)15;
         lists = qst + WS_NQS * sizeof(WsQuery);                           // u64[NQS][2][K]
         lists = (lists + 15) & ~(size_t)15;
         wbuf = lists + (size_t)WS_NQS * 2 * K * 8;                        // u64[SW][2][WBUF]
-        prq = wbuf + (size_t)WS_SW * 2 * WS_WBUF * 8;                     // f32[PD][G][d_pad]
+        prq = wbuf + (size_t)WS_SW * 2 * WS_WBUF * 8;                     // f32[PD][G][d_pad] (TMA-filled)
+        prq = (prq + 127) & ~(size_t)127;
         stage = prq + (size_t)WS_PD * G * d_pad * 4;                      // u8[SW][SD][32 * s_pad]
         stage = (stage + 127) & ~(size_t)127;
         stage_bytes = (size_t)32 * s_pad;
@@ -607,7 +616,7 @@ __device__ __forceinline__ void ws_scan_job(const ScanArgs& a, const WsJob* J, c
         const uint32_t src = sg.stage0 + st * sg.stage_bytes + lane * 16, cstride = (uint32_t)k.nb * 16;
         const uint32_t base = lut_s + k.g * lut_each;
         float acc = 0.f;
-        int c = 0;
+        int c = a.debug_skip_gather ? nch : 0;  // debug bit 1
         for (; c + 2 <= nfull; c += 2) {
             const uint4 w0 = lds128(src + c * cstride), w1 = lds128(src + (c + 1) * cstride);
             acc = ws_acc16<DT, LOGN>(acc, w0, base + (uint32_t)(c * 16 * N * E), 16, true);
@@ -633,46 +642,116 @@ __device__ __forceinline__ void ws_scan_job(const ScanArgs& a, const WsJob* J, c
                 pass = key < tau;
             }
         }
+        if (a.debug_skip_gather) pass = false;
         tk.offer(key, pass);
         if (tk.n > WS_WBUF - 32) tk.flush(S, qlist, K);
     }
     sg.top_up(a, jobs, full, cjob, lane);  // keep the ring busy into the next job(s)
 }
 
-// Prep warp: one job = up to G pending probes of query q (pq[from .. from+ng))
-// written into prep-ring entry job % PD (descriptor + padded residuals).
-__device__ __forceinline__ void ws_emit_job(const ScanArgs& a, WsJob* pjobs, float* prq, u64* pfull, u64* pempty,
-                                            int job, int G, int d_pad, int q, int qs, const WsPrepQ* pq, int from,
-                                            int ng, bool last, int lane) {
-    const int ps = job % WS_PD;
-    if (job >= WS_PD) mbar_wait(pempty + ps, ((job / WS_PD) - 1) & 1);
-    WsJob* J = pjobs + ps;
-    if (lane == 0) {
-        int pref = 0;
-        for (int g = 0; g < ng; ++g) {
-            J->lc[g] = pq->lc[from + g];
-            J->len[g] = pq->len[from + g];
-            J->off[g] = pq->off[from + g];
-            J->pref[g] = pref;
-            pref += (pq->len[from + g] + 31) >> 5;
-        }
-        J->pref[ng] = pref;
-        J->nblk = pref;
-        J->ng = ng;
-        J->q = q;
-        J->qs = qs;
-        J->last = last ? 1 : 0;
-    }
-    float* rq = prq + (size_t)ps * G * d_pad;
+// ---------------------------------------------------------------- planning
+// One warp per query: resolve the probe keys (32 at a time) to owned,
+// non-empty lists, group them G per job, and write each job's descriptor and
+// its G padded residual rows rq = fl(q - coarse[c]) to global memory, where
+// the search kernel's prep warp fetches them with two TMA bulk copies.
+// Also the query's job count and candidate count (all probes, owned or not).
+__global__ void __launch_bounds__(256) ws_plan_kernel(const ScanArgs a, int G, int d_pad, int JMAX, WsJob* jobs,
+                                                      float* rq, int* njobs, long long* ncand)
+#ifndef IVFPQ_DEFINE_PLAN_KERNEL
+    ;  // defined in ivfpq_b200.cu
+#else
+{
+    __shared__ int s_lc[8][32 + WS_MAX_G];
+    __shared__ int s_len[8][32 + WS_MAX_G];
+    __shared__ long long s_off[8][32 + WS_MAX_G];
+    const int wq = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int q = blockIdx.x * 8 + wq;
+    if (q >= a.nq) return;
+    int* lcq = s_lc[wq];
+    int* lenq = s_len[wq];
+    long long* offq = s_off[wq];
+    const u64* probes = a.probes + (size_t)q * a.P;
     const float* qv = a.queries + (size_t)q * a.d;
-    for (int g = 0; g < ng; ++g) {
-        const float* cv = a.coarse + (size_t)pq->lc[from + g] * a.d;
-        for (int x = lane; x < d_pad; x += 32)
-            rq[g * d_pad + x] = x < a.d ? __fsub_rn(__ldg(qv + x), __ldg(cv + x)) : 0.0f;
+    int pend = 0, nj = 0;
+    long long nc = 0;
+    auto emit = [&](int from, int ng, bool last) {
+        WsJob* J = jobs + (size_t)q * JMAX + nj;
+        if (lane == 0) {
+            int pref = 0;
+            for (int g = 0; g < ng; ++g) {
+                J->lc[g] = lcq[from + g];
+                J->len[g] = lenq[from + g];
+                J->off[g] = offq[from + g];
+                J->pref[g] = pref;
+                pref += (lenq[from + g] + 31) >> 5;
+            }
+            J->pref[ng] = pref;
+            J->nblk = pref;
+            J->ng = ng;
+            J->q = q;
+            J->qs = 0;
+            J->last = last ? 1 : 0;
+        }
+        float* r = rq + ((size_t)q * JMAX + nj) * G * d_pad;
+        for (int g = 0; g < ng; ++g) {
+            const float* cv = a.coarse + (size_t)lcq[from + g] * a.d;
+            for (int x = lane; x < d_pad; x += 32) r[g * d_pad + x] = x < a.d ? __fsub_rn(qv[x], cv[x]) : 0.0f;
+        }
+        ++nj;
+    };
+    for (int base = 0; base < a.P; base += 32) {
+        const int pi = base + lane;
+        const u64 key = pi < a.P ? probes[pi] : ~0ull;
+        const uint32_t gid = (uint32_t)key;
+        const int lc = key == ~0ull ? -1 : a.g2l[gid];
+        long long o = 0, len = 0, gl = key == ~0ull ? 0 : a.glen[gid];
+        if (lc >= 0) {
+            o = a.off[lc];
+            len = a.off[lc + 1] - o;
+        }
+        for (int sh = 16; sh; sh >>= 1) gl += __shfl_xor_sync(0xffffffffu, gl, sh);
+        nc += gl;
+        const unsigned m = __ballot_sync(0xffffffffu, len > 0);
+        if (len > 0) {
+            const int at = pend + __popc(m & ((1u << lane) - 1));
+            lcq[at] = lc;
+            lenq[at] = (int)len;
+            offq[at] = o;
+        }
+        pend += __popc(m);
+        __syncwarp();
+        const bool more = base + 32 < a.P;
+        int taken = 0;
+        // emit full jobs; keep >= 1 pending until the end so the final job is marked last
+        while (pend - taken > G || (!more && pend - taken > 0)) {
+            const int ng = min(G, pend - taken);
+            emit(taken, ng, !more && pend - taken == ng);
+            taken += ng;
+        }
+        const int rest = pend - taken;
+        int lc2 = 0, len2 = 0;
+        long long o2 = 0;
+        if (lane < rest) {
+            lc2 = lcq[taken + lane];
+            len2 = lenq[taken + lane];
+            o2 = offq[taken + lane];
+        }
+        __syncwarp();
+        if (lane < rest) {
+            lcq[lane] = lc2;
+            lenq[lane] = len2;
+            offq[lane] = o2;
+        }
+        __syncwarp();
+        pend = rest;
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(pfull + ps);
+    if (nj == 0) emit(0, 0, true);  // no owned non-empty list: one empty last job
+    if (lane == 0) {
+        njobs[q] = nj;
+        ncand[q] = nc;
+    }
 }
+#endif
 
 template <int DT, int LOGN, int SUB_D>
 __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) {
@@ -696,7 +775,6 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
     u64* lists = reinterpret_cast<u64*>(smem + L.lists);
     float* prq = reinterpret_cast<float*>(smem + L.prq);
     uint8_t* lut_all = smem + L.lut;
-    WsPrepQ* pq = reinterpret_cast<WsPrepQ*>(smem + L.prepq);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if ((smem_addr(lut_all) & 255u) != 0u) __trap();  // PRMT LUT addressing needs 256-byte alignment
 
@@ -736,20 +814,22 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
 
     if (warp == WS_PREP_WARP) {
         // ============================ prep warp ============================
-        // Hands out queries, resolves probe keys to (local list, offset,
-        // length) 32 at a time, and writes job descriptors + residuals
-        // rq = fl(q - coarse[c]) into the slots, one job ahead of the builders.
+        // Hands out queries and streams their planned jobs (descriptor +
+        // residual rows, from ws_plan_kernel) into the prep ring with TMA bulk
+        // copies, up to WS_PD jobs ahead of the builders.
+        int* pqs = reinterpret_cast<int*>(smem + L.prepq);
+        const uint32_t pjob_bytes = (uint32_t)sizeof(WsJob), prq_bytes = (uint32_t)(G * d_pad * 4);
         int job = 0, qseq = -1;
         while (true) {
             int q = 0;
             if (lane == 0) q = atomicAdd(w.work, 1);
             q = __shfl_sync(0xffffffffu, q, 0);
+            const int ps0 = job % WS_PD;
             if (q >= a.nq) {
-                const int ps = job % WS_PD;
-                if (job >= WS_PD) mbar_wait(pempty + ps, ((job / WS_PD) - 1) & 1);
+                if (job >= WS_PD) mbar_wait(pempty + ps0, ((job / WS_PD) - 1) & 1);
                 if (lane == 0) {
-                    pjobs[ps].qs = -1;
-                    mbar_arrive(pfull + ps);
+                    pqs[ps0] = -1;
+                    mbar_arrive(pfull + ps0);
                 }
                 break;
             }
@@ -758,67 +838,22 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
             WsQuery* S = qst + qs;
             // the state is reused only after the query that last held it was finalised
             if (qseq >= NQS) mbar_wait(reinterpret_cast<u64*>(smem + L.qfree) + qs, ((qseq / NQS) - 1) & 1);
+            const int nj = w.plan_njobs[q];
             if (lane == 0) {
                 S->q = q;
-                S->ncand = 0;
+                S->ncand = w.plan_ncand[q];
             }
-            const u64* probes = a.probes + (size_t)q * a.P;
-            int nq_pend = 0;  // valid probes waiting in pq (warp-uniform)
-            for (int base = 0; base < a.P; base += 32) {
-                const int pi = base + lane;
-                u64 key = pi < a.P ? probes[pi] : ~0ull;
-                const uint32_t gid = (uint32_t)key;
-                const int lc = key == ~0ull ? -1 : a.g2l[gid];
-                long long o = 0, len = 0, gl = 0;
-                if (key != ~0ull) gl = a.glen[gid];
-                if (lc >= 0) {
-                    o = a.off[lc];
-                    len = a.off[lc + 1] - o;
+            for (int j = 0; j < nj; ++j, ++job) {
+                const int ps = job % WS_PD;
+                if (job >= WS_PD) mbar_wait(pempty + ps, ((job / WS_PD) - 1) & 1);
+                if (lane == 0) {
+                    pqs[ps] = qs;
+                    const size_t gj = (size_t)q * w.JMAX + j;
+                    fence_proxy_async();  // builders' reads of this entry before the async overwrite
+                    mbar_expect_tx(pfull + ps, pjob_bytes + prq_bytes);
+                    bulk_g2s(smem_addr(pjobs + ps), w.plan_jobs + gj, pjob_bytes, pfull + ps);
+                    bulk_g2s(smem_addr(prq + (size_t)ps * G * d_pad), w.plan_rq + gj * G * d_pad, prq_bytes, pfull + ps);
                 }
-                // candidate count of every probe, owned or not
-                for (int sh = 16; sh; sh >>= 1) gl += __shfl_xor_sync(0xffffffffu, gl, sh);
-                if (lane == 0) S->ncand += gl;
-                const bool valid = len > 0;
-                const unsigned m = __ballot_sync(0xffffffffu, valid);
-                if (valid) {
-                    const int at = nq_pend + __popc(m & ((1u << lane) - 1));
-                    pq->lc[at] = lc;
-                    pq->len[at] = (int)len;
-                    pq->off[at] = o;
-                }
-                nq_pend += __popc(m);
-                __syncwarp();
-                const bool more = base + 32 < a.P;
-                // emit full jobs; keep >= 1 pending so the final job knows it is last
-                int taken = 0;
-                while (nq_pend - taken > G || (!more && nq_pend - taken > 0)) {
-                    const int ng = min(G, nq_pend - taken);
-                    const bool last = !more && nq_pend - taken == ng;
-                    ws_emit_job(a, pjobs, prq, pfull, pempty, job, G, d_pad, q, qs, pq, taken, ng, last, lane);
-                    taken += ng;
-                    ++job;
-                }
-                if (!more && nq_pend == 0) {  // no owned non-empty list: an empty last job
-                    ws_emit_job(a, pjobs, prq, pfull, pempty, job, G, d_pad, q, qs, pq, 0, 0, true, lane);
-                    ++job;
-                }
-                // compact the pending queue
-                const int rest = nq_pend - taken;
-                int lc2 = 0, len2 = 0;
-                long long o2 = 0;
-                if (lane < rest) {
-                    lc2 = pq->lc[taken + lane];
-                    len2 = pq->len[taken + lane];
-                    o2 = pq->off[taken + lane];
-                }
-                __syncwarp();
-                if (lane < rest) {
-                    pq->lc[lane] = lc2;
-                    pq->len[lane] = len2;
-                    pq->off[lane] = o2;
-                }
-                __syncwarp();
-                nq_pend = rest;
             }
         }
     } else if (warp < WS_BW) {
@@ -834,17 +869,21 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
             mbar_wait(pfull + ps, (job / WS_PD) & 1);
             if (wrapped) mbar_wait(empty + slot, eph);
             const WsJob* PJ = pjobs + ps;
+            const int pq_s = reinterpret_cast<const int*>(smem + L.prepq)[ps];
             if (t < 32) {  // the descriptor travels with the LUT slot (warp 0 copies it)
                 const int* src = reinterpret_cast<const int*>(PJ);
                 int* dst = reinterpret_cast<int*>(jobs + slot);
                 for (int i = t; i < (int)(sizeof(WsJob) / 4); i += 32) dst[i] = src[i];
+                __syncwarp();
+                if (t == 0) jobs[slot].qs = pq_s;
             }
-            if (PJ->qs < 0) {
+            if (pq_s < 0) {
                 mbar_arrive(full + slot);
                 break;
             }
-            B.build(prq_s + (uint32_t)(ps * G * d_pad * 4), (uint32_t)(d_pad * 4), lut_s + (uint32_t)(slot * G * lut_each),
-                    (uint32_t)lut_each, PJ->ng, jpt);
+            if (!(w.debug & 1))
+                B.build(prq_s + (uint32_t)(ps * G * d_pad * 4), (uint32_t)(d_pad * 4),
+                        lut_s + (uint32_t)(slot * G * lut_each), (uint32_t)lut_each, PJ->ng, jpt);
             mbar_arrive(pempty + ps);
             mbar_arrive(full + slot);
             if (++slot == NBUF) {
@@ -885,7 +924,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
             WsQuery* S = qst + qs;
             u64* qlist = lists + (size_t)qs * 2 * K;
             const uint8_t* lutb = lut_all + (size_t)slot * G * lut_each;  // rows padded; scan reads j < s
-            ws_scan_job<DT, LOGN>(a, J, jobs, full, job, sw, lane, smem_addr(lutb), (uint32_t)lut_each, S, qlist, K, tk, sg);
+            if (!(w.debug & 4))
+                ws_scan_job<DT, LOGN>(a, J, jobs, full, job, sw, lane, smem_addr(lutb), (uint32_t)lut_each, S, qlist, K,
+                                      tk, sg);
             if (J->last) {
                 if (tk.n > 0) tk.flush(S, qlist, K);
                 int d = 0;
