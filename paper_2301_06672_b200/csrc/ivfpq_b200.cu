@@ -46,6 +46,7 @@ int set_err(int code, const char* fmt, ...) {
     } while (0)
 
 std::atomic<long long> g_launches{0};
+unsigned long long* g_ws_prof = nullptr;  // debug profiling buffer (IVFPQ_WS_DEBUG bit 5)
 
 // After every kernel launch: count it (ivfpq_launch_count) and check it.
 #define KCHECK()                                              \
@@ -67,7 +68,7 @@ constexpr size_t COARSE_CHUNK_BYTES = 256ull << 20;
 size_t lut_budget_bytes() {
     static size_t v = [] {
         const char* e = getenv("IVFPQ_LUT_BUDGET_KB");
-        return (size_t)(e ? atoi(e) : 32) * 1024;
+        return (size_t)(e ? atoi(e) : 64) * 1024;
     }();
     return v;
 }
@@ -438,6 +439,8 @@ int run_scan(ivfpq_index* idx, const float* d_q, int64_t nq, const uint64_t* d_p
     a.K = (int)K;
     a.G = G;
     a.debug_skip_gather = 0;
+    a.debug_skip_copy = 0;
+    a.debug_skip_ids = 0;
     a.out_keys = out_keys;
     a.out_ncand = out_ncand;
     a.out_ids = out_ids;
@@ -459,6 +462,17 @@ int run_scan(ivfpq_index* idx, const float* d_q, int64_t nq, const uint64_t* d_p
         }();
         w.debug = dbg;
         w.a.debug_skip_gather = (dbg & 2) != 0;
+        w.a.debug_skip_copy = (dbg & 8) != 0;
+        w.a.debug_skip_ids = (dbg & 16) != 0;
+        w.prof = nullptr;
+        if (dbg & 32) {
+            static unsigned long long* prof = nullptr;
+            const size_t pb = (size_t)idx->num_sms * 32 * 8 * 8;
+            if (!prof) CK(cudaMalloc((void**)&prof, pb));
+            CK(cudaMemsetAsync(prof, 0, pb, st));
+            w.prof = prof;
+            g_ws_prof = prof;
+        }
         CKR(idx->work.ensure(16));
         w.work = idx->work.as<int>();
         CK(cudaMemsetAsync(w.work, 0, sizeof(int), st));
@@ -532,6 +546,14 @@ int ivfpq_max_k(void) { return MAX_K; }
 int ivfpq_set_scan_kernel(int mode) {
     if (mode < 0 || mode > 1) return set_err(IVFPQ_EINVAL, "scan kernel mode must be 0 (auto) or 1 (v1)");
     g_scan_mode.store(mode);
+    return IVFPQ_OK;
+}
+
+// Debug: copy the per-warp cycle counters of the last profiled launch.
+extern "C" int ivfpq_debug_ws_prof(void* host, int64_t bytes) {
+    if (!g_ws_prof) return set_err(IVFPQ_EINVAL, "no profiled launch");
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(host, g_ws_prof, bytes, cudaMemcpyDeviceToHost));
     return IVFPQ_OK;
 }
 

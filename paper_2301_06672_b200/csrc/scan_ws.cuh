@@ -38,8 +38,12 @@
 
 namespace ivfpq {
 
-constexpr int WS_BW = 16;                    // builder warps (4 TMEM column groups)
-constexpr int WS_SW = 15;                    // scanner warps
+#ifndef WS_BW_CFG
+#define WS_BW_CFG 8
+#define WS_SW_CFG 11
+#endif
+constexpr int WS_BW = WS_BW_CFG;             // builder warps (WS_BW/4 TMEM column groups)
+constexpr int WS_SW = WS_SW_CFG;             // scanner warps
 constexpr int WS_NB = WS_BW * 32;            // 512 builder threads
 constexpr int WS_PREP_WARP = WS_BW + WS_SW;   // warp 31: job preparation
 // Builder row geometry (shared by host plan and device): a builder thread owns
@@ -70,6 +74,7 @@ struct WsArgs {
     int debug;             // perf experiments only (wrong results): bit 0 = skip LUT math, bit 1 = skip
                            // gathers + offers, bit 2 = scanners skip their blocks entirely
     int* work;             // global query counter (zeroed before launch)
+    unsigned long long* prof;  // debug bit 5: per-(CTA, warp) cycle counters [grid][32][8], else null
 };
 
 struct WsJob {
@@ -428,16 +433,33 @@ struct WarpTopK {
         n += __popc(m);
     }
 
-    // Merge the buffer into the query's shared list (lock held by this warp).
+    // Merge the buffer into the query's shared list.  Candidates are first
+    // re-filtered against the current threshold (it has usually tightened
+    // since they were offered), so most flushes end without taking the lock.
     __device__ void flush(WsQuery* S, u64* lists, int K) {
         const int lane = threadIdx.x & 31;
         __syncwarp();
-        for (int i = lane; i < n; i += 32) {
-            const u64 x = buf[i];
-            int r = 0;
-            for (int j = 0; j < n; ++j) r += buf[j] < x;
-            srt[r] = x;
+        const u64 tau = *(volatile u64*)&S->tau;
+        int m = 0;
+        for (int i0 = 0; i0 < n; i0 += 32) {
+            const u64 x = i0 + lane < n ? buf[i0 + lane] : ~0ull;
+            const bool keep = x < tau;
+            const unsigned bm = __ballot_sync(0xffffffffu, keep);
+            if (keep) srt[m + __popc(bm & ((1u << lane) - 1))] = x;
+            m += __popc(bm);
         }
+        n = 0;
+        if (m == 0) return;
+        __syncwarp();
+        for (int i = lane; i < m; i += 32) {
+            const u64 x = srt[i];
+            int r = 0;
+            for (int j = 0; j < m; ++j) r += srt[j] < x;
+            buf[r] = x;
+        }
+        __syncwarp();
+        for (int i = lane; i < m; i += 32) srt[i] = buf[i];
+        const int n = m;
         if (lane == 0) {
             while (atomicCAS(&S->lock, 0, 1) != 0) {
             }
@@ -465,7 +487,6 @@ struct WarpTopK {
             atomicExch(&S->lock, 0);
         }
         __syncwarp();
-        n = 0;
     }
 };
 
@@ -528,17 +549,36 @@ __device__ __forceinline__ float ws_acc16(float acc, uint4 w, uint32_t base, int
     return acc;
 }
 
-// Block k of a job for scanner warp sw is job block b = sw + k*SW: pair g
-// (found incrementally), vectors [vstart, vstart+nb) of list J->lc[g].
-struct WsBlk {
-    int g, nb;
+// Block table of one job for one scanner warp, held lane-parallel: lane l
+// describes the warp's block k0 + l (job block b = sw + (k0 + l) * SW), i.e.
+// pair g and vectors [vo, vo + nb) of that pair's list.  Built once per job
+// (and per 32 blocks); per block the consumer/producer only shuffle.
+struct WsTab {
+    int g, nb, n, k0;
     long long vo;
+    __device__ __forceinline__ void load(const WsJob* J, int sw, int lane, int k0_) {
+        const int nblk = J->nblk, ng = J->ng;
+        k0 = k0_;
+        n = nblk > sw ? (nblk - sw + WS_SW - 1) / WS_SW : 0;
+        const int b = sw + (k0 + lane) * WS_SW;
+        g = 0;
+        nb = 0;
+        vo = 0;
+        if (b < nblk) {
+            while (g + 1 < ng && b >= J->pref[g + 1]) ++g;
+            const int vstart = (b - J->pref[g]) * 32;
+            nb = min(32, J->len[g] - vstart);
+            vo = J->off[g] + vstart;
+        }
+    }
+    // block k of the warp (caller reloads the window when k - k0 >= 32)
+    __device__ __forceinline__ void get(int k, int& gk, int& nbk, long long& vok) const {
+        const int l = k - k0;
+        gk = __shfl_sync(0xffffffffu, g, l);
+        nbk = __shfl_sync(0xffffffffu, nb, l);
+        vok = __shfl_sync(0xffffffffu, vo, l);
+    }
 };
-__device__ __forceinline__ WsBlk ws_blk(const WsJob* J, int ng, int b, int g) {
-    while (g + 1 < ng && b >= J->pref[g + 1]) ++g;
-    const int vstart = (b - J->pref[g]) * 32;
-    return WsBlk{g, min(32, J->len[g] - vstart), J->off[g] + vstart};
-}
 
 // Per-warp ring of SD code-block stages filled by TMA bulk copies.  The
 // producer side (lane 0) runs ahead of the consumer across job boundaries:
@@ -552,26 +592,26 @@ struct WsStager {
     int SD, NBUF, sw;
     int issued, consumed; // blocks
     int ps, cs, cph;      // producer stage, consumer stage, consumer phase (no runtime div/mod)
-    int pjob, pb, pg;     // producer cursor: job, block index, pair hint
+    int pjob, pk;         // producer cursor: job, warp-block index
     int pslot, pph;       // LUT slot of pjob and its full-barrier phase
     bool pready, pend;
-    const WsJob* PJ;
+    WsTab ptab;
 
     __device__ __forceinline__ void top_up(const ScanArgs& a, const WsJob* jobs, u64* full, int cjob, int lane) {
         while (issued - consumed < SD && !pend) {
             if (!pready) {
                 if (pjob >= cjob + NBUF) return;
                 if (pjob != cjob && !mbar_test(full + pslot, pph)) return;
-                PJ = jobs + pslot;
-                pready = true;
-                pb = sw;
-                pg = 0;
+                const WsJob* PJ = jobs + pslot;
                 if (PJ->qs < 0) {
                     pend = true;
                     return;
                 }
+                ptab.load(PJ, sw, lane, 0);
+                pk = 0;
+                pready = true;
             }
-            if (pb >= PJ->nblk) {
+            if (pk >= ptab.n) {
                 ++pjob;
                 if (++pslot == NBUF) {
                     pslot = 0;
@@ -580,18 +620,20 @@ struct WsStager {
                 pready = false;
                 continue;
             }
-            const WsBlk k = ws_blk(PJ, PJ->ng, pb, pg);
-            pg = k.g;
-            if (lane == 0) {
-                const int st = ps;
-                const uint32_t bytes = (uint32_t)k.nb * (uint32_t)a.s_pad;
-                fence_proxy_async();  // earlier generic reads of this stage before the async overwrite
-                mbar_expect_tx(sbar + st, bytes);
-                bulk_g2s(stage0 + st * stage_bytes, a.codes + (size_t)k.vo * a.s_pad, bytes, sbar + st);
+            if (pk - ptab.k0 >= 32) ptab.load(jobs + pslot, sw, lane, pk);
+            int g, nb;
+            long long vo;
+            ptab.get(pk, g, nb, vo);
+            if (lane == 0 && !a.debug_skip_copy) {
+                const uint32_t bytes = (uint32_t)nb * (uint32_t)a.s_pad;
+                // the stage's previous contents were consumed (values used, then
+                // __syncwarp) before this point in program order
+                mbar_expect_tx(sbar + ps, bytes);
+                bulk_g2s(stage0 + ps * stage_bytes, a.codes + (size_t)vo * a.s_pad, bytes, sbar + ps);
             }
             ++issued;
             ps = ps + 1 == SD ? 0 : ps + 1;
-            pb += WS_SW;
+            ++pk;
         }
     }
 };
@@ -602,19 +644,47 @@ struct WsStager {
 template <int DT, int LOGN>
 __device__ __forceinline__ void ws_scan_job(const ScanArgs& a, const WsJob* J, const WsJob* jobs, u64* full, int cjob,
                                             int sw, int lane, uint32_t lut_s, uint32_t lut_each, WsQuery* S,
-                                            u64* qlist, int K, WarpTopK& tk, WsStager& sg) {
+                                            u64* qlist, int K, WarpTopK& tk, WsStager& sg,
+                                            unsigned long long* prof) {
     constexpr int N = 1 << LOGN;
     constexpr int E = (int)sizeof(typename LutTraits<DT>::T);
-    const int nch = a.s_pad >> 4, nfull = a.s >> 4, ng = J->ng, nblk = J->nblk;
-    int g = 0;
-    for (int b = sw; b < nblk; b += WS_SW) {
-        sg.top_up(a, jobs, full, cjob, lane);
-        const WsBlk k = ws_blk(J, ng, b, g);
-        g = k.g;
+    const int nch = a.s_pad >> 4, nfull = a.s >> 4;
+#ifdef IVFPQ_WS_FINE_PROF  // fine-grained per-block timers (build with -DIVFPQ_WS_FINE_PROF)
+#define WS_P0() _p0 = prof ? clock64() : 0
+#define WS_PA(slot) \
+    do { \
+        if (prof && lane == 0) prof[slot] += (unsigned long long)(clock64() - _p0); \
+    } while (0)
+#else
+#define WS_P0() (void)_p0
+#define WS_PA(slot) (void)prof
+#endif
+    WsTab ct;
+    ct.load(J, sw, lane, 0);
+    long long _p0 = 0;
+    for (int k = 0; k < ct.n; ++k) {
+        if (k - ct.k0 >= 32) ct.load(J, sw, lane, k);
+        {
+            WS_P0();
+            sg.top_up(a, jobs, full, cjob, lane);
+            WS_PA(3);
+        }
+        WS_P0();
+        int g, nb;
+        long long vo;
+        ct.get(k, g, nb, vo);
+        // the id is fetched up front; the table lookups below hide its latency
+        const uint32_t id = lane < nb ? (a.debug_skip_ids ? (uint32_t)(vo + lane) : __ldg(a.ids + vo + lane)) : 0u;
         const int st = sg.cs;
-        mbar_wait(sg.sbar + st, sg.cph);
-        const uint32_t src = sg.stage0 + st * sg.stage_bytes + lane * 16, cstride = (uint32_t)k.nb * 16;
-        const uint32_t base = lut_s + k.g * lut_each;
+        WS_PA(4);
+        {
+            WS_P0();
+            if (!a.debug_skip_copy) mbar_wait(sg.sbar + st, sg.cph);
+            WS_PA(5);
+        }
+        WS_P0();
+        const uint32_t src = sg.stage0 + st * sg.stage_bytes + lane * 16, cstride = (uint32_t)nb * 16;
+        const uint32_t base = lut_s + g * lut_each;
         float acc = 0.f;
         int c = a.debug_skip_gather ? nch : 0;  // debug bit 1
         for (; c + 2 <= nfull; c += 2) {
@@ -627,27 +697,32 @@ __device__ __forceinline__ void ws_scan_job(const ScanArgs& a, const WsJob* J, c
             acc = ws_acc16<DT, LOGN>(acc, w0, base + (uint32_t)(c * 16 * N * E), a.s - 16 * c, c < nfull);
         }
         __syncwarp();
+        WS_PA(6);
+        WS_P0();
         ++sg.consumed;
         if (++sg.cs == sg.SD) {
             sg.cs = 0;
             sg.cph ^= 1;
         }
-        u64 key = ~0ull;
-        bool pass = false;
-        if (lane < k.nb) {
-            const uint32_t rb = __float_as_uint(lut_finish<DT>(acc));
-            const u64 tau = *(volatile u64*)&S->tau;
-            if (rb <= (uint32_t)(tau >> 32)) {
-                key = ((u64)rb << 32) | a.ids[k.vo + lane];
-                pass = key < tau;
-            }
-        }
-        if (a.debug_skip_gather) pass = false;
+        const uint32_t rb = __float_as_uint(lut_finish<DT>(acc));
+        const u64 tau = *(volatile u64*)&S->tau;
+        const u64 key = ((u64)rb << 32) | id;
+        const bool pass = lane < nb && key < tau && !a.debug_skip_gather;
         tk.offer(key, pass);
         if (tk.n > WS_WBUF - 32) tk.flush(S, qlist, K);
+        WS_PA(7);
     }
     sg.top_up(a, jobs, full, cjob, lane);  // keep the ring busy into the next job(s)
+#undef WS_P0
+#undef WS_PA
 }
+
+// debug profiling: accumulate clock64 deltas per warp (lane 0) into w.prof
+#define WS_T0() const long long _t0 = w.prof ? clock64() : 0
+#define WS_ACC(slot) \
+    do { \
+        if (w.prof && lane == 0) atomicAdd(w.prof + ((size_t)blockIdx.x * 32 + warp) * 8 + (slot), (unsigned long long)(clock64() - _t0)); \
+    } while (0)
 
 // ---------------------------------------------------------------- planning
 // One warp per query: resolve the probe keys (32 at a time) to owned,
@@ -795,10 +870,10 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
     if (threadIdx.x == 0) {
         for (int b = 0; b < WS_PD; ++b) {
             mbar_init(pfull + b, 1);
-            mbar_init(pempty + b, WS_NB);
+            mbar_init(pempty + b, WS_BW);  // one arrival per builder warp
         }
         for (int b = 0; b < NBUF; ++b) {
-            mbar_init(full + b, WS_NB);
+            mbar_init(full + b, WS_BW);
             mbar_init(empty + b, WS_SW);
         }
         u64* sb = reinterpret_cast<u64*>(smem + L.sbars);
@@ -845,7 +920,11 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
             }
             for (int j = 0; j < nj; ++j, ++job) {
                 const int ps = job % WS_PD;
-                if (job >= WS_PD) mbar_wait(pempty + ps, ((job / WS_PD) - 1) & 1);
+                {
+                    WS_T0();
+                    if (job >= WS_PD) mbar_wait(pempty + ps, ((job / WS_PD) - 1) & 1);
+                    WS_ACC(0);
+                }
                 if (lane == 0) {
                     pqs[ps] = qs;
                     const size_t gj = (size_t)q * w.JMAX + j;
@@ -866,8 +945,16 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
         bool wrapped = false;
         for (int job = 0;; ++job) {
             const int ps = job % WS_PD;
-            mbar_wait(pfull + ps, (job / WS_PD) & 1);
-            if (wrapped) mbar_wait(empty + slot, eph);
+            {
+                WS_T0();
+                mbar_wait(pfull + ps, (job / WS_PD) & 1);
+                WS_ACC(0);
+            }
+            {
+                WS_T0();
+                if (wrapped) mbar_wait(empty + slot, eph);
+                WS_ACC(1);
+            }
             const WsJob* PJ = pjobs + ps;
             const int pq_s = reinterpret_cast<const int*>(smem + L.prepq)[ps];
             if (t < 32) {  // the descriptor travels with the LUT slot (warp 0 copies it)
@@ -878,14 +965,22 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
                 if (t == 0) jobs[slot].qs = pq_s;
             }
             if (pq_s < 0) {
-                mbar_arrive(full + slot);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(full + slot);
                 break;
             }
-            if (!(w.debug & 1))
-                B.build(prq_s + (uint32_t)(ps * G * d_pad * 4), (uint32_t)(d_pad * 4),
-                        lut_s + (uint32_t)(slot * G * lut_each), (uint32_t)lut_each, PJ->ng, jpt);
-            mbar_arrive(pempty + ps);
-            mbar_arrive(full + slot);
+            {
+                WS_T0();
+                if (!(w.debug & 1))
+                    B.build(prq_s + (uint32_t)(ps * G * d_pad * 4), (uint32_t)(d_pad * 4),
+                            lut_s + (uint32_t)(slot * G * lut_each), (uint32_t)lut_each, PJ->ng, jpt);
+                WS_ACC(2);
+            }
+            __syncwarp();  // the warp's LUT stores / prep reads are ordered before its lane-0 arrivals
+            if (lane == 0) {
+                mbar_arrive(pempty + ps);
+                mbar_arrive(full + slot);
+            }
             if (++slot == NBUF) {
                 slot = 0;
                 if (wrapped) eph ^= 1;
@@ -899,6 +994,11 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
         const int sw = warp - WS_BW;
         u64* wb = reinterpret_cast<u64*>(smem + L.wbuf) + (size_t)sw * 2 * WS_WBUF;
         WarpTopK tk{wb, wb + WS_WBUF, 0};
+#ifdef IVFPQ_WS_FINE_PROF
+        unsigned long long wprof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#else
+        unsigned long long* wprof = nullptr;
+#endif
         WsStager sg;
         sg.stage0 = smem_addr(smem + L.stage) + (uint32_t)(sw * SD * L.stage_bytes);
         sg.stage_bytes = (uint32_t)L.stage_bytes;
@@ -910,23 +1010,36 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
         sg.ps = sg.cs = sg.cph = 0;
         sg.pslot = sg.pph = 0;
         sg.pjob = 0;
-        sg.pb = sw;
-        sg.pg = 0;
+        sg.pk = 0;
         sg.pready = false;
         sg.pend = false;
-        sg.PJ = nullptr;
         int slot = 0, fph = 0;
         for (int job = 0;; ++job) {
-            mbar_wait(full + slot, fph);
+            {
+                WS_T0();
+                mbar_wait(full + slot, fph);
+                WS_ACC(0);
+            }
             const WsJob* J = jobs + slot;
             const int qs = J->qs;
-            if (qs < 0) break;
+            if (qs < 0) {
+#ifdef IVFPQ_WS_FINE_PROF
+                if (w.prof && lane == 0)
+                    for (int i = 3; i < 8; ++i) atomicAdd(w.prof + ((size_t)blockIdx.x * 32 + warp) * 8 + i, wprof[i]);
+#endif
+                break;
+            }
             WsQuery* S = qst + qs;
             u64* qlist = lists + (size_t)qs * 2 * K;
             const uint8_t* lutb = lut_all + (size_t)slot * G * lut_each;  // rows padded; scan reads j < s
-            if (!(w.debug & 4))
-                ws_scan_job<DT, LOGN>(a, J, jobs, full, job, sw, lane, smem_addr(lutb), (uint32_t)lut_each, S, qlist, K,
-                                      tk, sg);
+            {
+                WS_T0();
+                if (!(w.debug & 4))
+                    ws_scan_job<DT, LOGN>(a, J, jobs, full, job, sw, lane, smem_addr(lutb), (uint32_t)lut_each, S, qlist,
+                                          K, tk, sg, w.prof ? wprof : nullptr);
+                WS_ACC(1);
+            }
+            WS_T0();
             if (J->last) {
                 if (tk.n > 0) tk.flush(S, qlist, K);
                 int d = 0;
@@ -966,6 +1079,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(empty + slot);
+            WS_ACC(2);
             if (++slot == NBUF) {
                 slot = 0;
                 fph ^= 1;
