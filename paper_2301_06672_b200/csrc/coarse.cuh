@@ -92,3 +92,169 @@ select_probes_kernel(const float* __restrict__ D, int nc, const int32_t* __restr
 }
 
 }  // namespace ivfpq
+
+namespace ivfpq {
+
+// ---------------------------------------------------------------------------
+// Fused K1: exact distances + per-query top-P in one kernel (P <= CT_MAXP).
+//
+// CTA = 64 queries x one slice of centroids, walked in tiles of 64.  Per tile
+// a thread computes a 4x4 micro-tile with packed f32x2 sub/mul (one rounding
+// each, as numpy) and scalar adds (sequential in t; scalar so that ptxas
+// cannot contract the f32x2 multiply into an FFMA2).  Keys
+// (d2 bits << 32 | global id) under the query's running P-th key are
+// appended to the query's buffer; after each tile one warp per query
+// rank-sorts the buffer and merges it into the query's sorted list.  Slices
+// are merged by merge_keys_kernel.  No distance matrix touches HBM.
+constexpr int CT_BQ = 64, CT_BC = 64, CT_BK = 16, CT_MAXP = 64;
+
+struct CoarseTopkArgs {
+    const float* Q;
+    const float* C;
+    const int32_t* l2g;
+    uint64_t* out;  // [nslices][nq][P]
+    int nq, nc, d, P, slice;
+};
+
+__host__ __device__ inline size_t coarse_topk_smem(int P) {
+    return (size_t)CT_BQ * (2 * P + CT_BC) * 8 + (size_t)CT_BQ * 16;
+}
+
+__device__ __forceinline__ unsigned long long ct_pk2(float a, float b) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void ct_upk2(unsigned long long v, float& a, float& b) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ unsigned long long ct_sub2(unsigned long long a, unsigned long long b) {
+    unsigned long long r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ unsigned long long ct_mul2(unsigned long long a, unsigned long long b) {
+    unsigned long long r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+
+__global__ void __launch_bounds__(256) coarse_topk_kernel(const CoarseTopkArgs a) {
+    __shared__ __align__(16) float Qs[CT_BK][CT_BQ + 4];
+    __shared__ __align__(16) float Cs[CT_BK][CT_BC + 4];
+    extern __shared__ __align__(16) uint8_t ct_smem[];
+    const int P = a.P;
+    uint64_t* lists = reinterpret_cast<uint64_t*>(ct_smem);          // [BQ][2][P]
+    uint64_t* buf = lists + (size_t)CT_BQ * 2 * P;                     // [BQ][BC]
+    int* cnt = reinterpret_cast<int*>(buf + (size_t)CT_BQ * CT_BC);   // [BQ]
+    int* cur = cnt + CT_BQ;                                            // [BQ]
+    uint64_t* tau = reinterpret_cast<uint64_t*>(cur + CT_BQ);          // [BQ]
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int q0 = blockIdx.y * CT_BQ;
+    const int cb = blockIdx.x * a.slice, ce = min(a.nc, cb + a.slice);
+    for (int i = threadIdx.x; i < CT_BQ * 2 * P; i += 256) lists[i] = ~0ull;
+    if (threadIdx.x < CT_BQ) {
+        cnt[threadIdx.x] = 0;
+        cur[threadIdx.x] = 0;
+        tau[threadIdx.x] = ~0ull;
+    }
+    __syncthreads();
+
+    for (int c0 = cb; c0 < ce; c0 += CT_BC) {
+        float acc[4][4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
+        for (int k0 = 0; k0 < a.d; k0 += CT_BK) {
+            for (int i = threadIdx.x; i < CT_BQ * CT_BK; i += 256) {
+                const int r = i / CT_BK, kk = i % CT_BK;
+                const int qr = q0 + r, cr = c0 + r, kd = k0 + kk;
+                Qs[kk][r] = (qr < a.nq && kd < a.d) ? a.Q[(size_t)qr * a.d + kd] : 0.0f;
+                Cs[kk][r] = (cr < ce && kd < a.d) ? a.C[(size_t)cr * a.d + kd] : 0.0f;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int kk = 0; kk < CT_BK; ++kk) {
+                const float4 qv = *reinterpret_cast<const float4*>(&Qs[kk][ty * 4]);
+                const float4 cv = *reinterpret_cast<const float4*>(&Cs[kk][tx * 4]);
+                const float qa[4] = {qv.x, qv.y, qv.z, qv.w};
+                const unsigned long long c01 = ct_pk2(cv.x, cv.y), c23 = ct_pk2(cv.z, cv.w);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const unsigned long long qq = ct_pk2(qa[i], qa[i]);
+                    const unsigned long long d01 = ct_sub2(c01, qq), d23 = ct_sub2(c23, qq);
+                    float s0, s1, s2, s3;
+                    ct_upk2(ct_mul2(d01, d01), s0, s1);
+                    ct_upk2(ct_mul2(d23, d23), s2, s3);
+                    acc[i][0] = __fadd_rn(acc[i][0], s0);
+                    acc[i][1] = __fadd_rn(acc[i][1], s1);
+                    acc[i][2] = __fadd_rn(acc[i][2], s2);
+                    acc[i][3] = __fadd_rn(acc[i][3], s3);
+                }
+            }
+            __syncthreads();
+        }
+        // candidates under the query's running P-th key
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int ql = ty * 4 + i;
+            const uint64_t t = tau[ql];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int c = c0 + tx * 4 + j;
+                if (c < ce) {
+                    const uint64_t key = ((uint64_t)__float_as_uint(acc[i][j]) << 32) | (uint32_t)a.l2g[c];
+                    if (key < t) buf[(size_t)ql * CT_BC + atomicAdd(&cnt[ql], 1)] = key;
+                }
+            }
+        }
+        __syncthreads();
+        // merge: one warp per query
+        for (int ql = warp; ql < CT_BQ; ql += 8) {
+            const int n = cnt[ql];
+            if (n == 0) continue;
+            uint64_t* b = buf + (size_t)ql * CT_BC;
+            // rank-sort the candidates (keys unique: distinct centroid ids)
+            uint64_t x0 = lane < n ? b[lane] : ~0ull, x1 = lane + 32 < n ? b[lane + 32] : ~0ull;
+            int r0 = 0, r1 = 0;
+            for (int j = 0; j < n; ++j) {
+                const uint64_t y = b[j];
+                r0 += y < x0;
+                r1 += y < x1;
+            }
+            __syncwarp();
+            if (lane < n) b[r0] = x0;
+            if (lane + 32 < n) b[r1] = x1;
+            __syncwarp();
+            const uint64_t* A = lists + ((size_t)ql * 2 + cur[ql]) * P;
+            uint64_t* O = lists + ((size_t)ql * 2 + (cur[ql] ^ 1)) * P;
+            for (int i = lane; i < P; i += 32) {
+                const uint64_t v = A[i];
+                const int pos = i + lower_bound_u64(b, n, v);
+                if (pos < P) O[pos] = v;
+            }
+            for (int i = lane; i < n; i += 32) {
+                const uint64_t v = b[i];
+                const int pos = i + lower_bound_u64(A, P, v);
+                if (pos < P) O[pos] = v;
+            }
+            __syncwarp();
+            if (lane == 0) {
+                cur[ql] ^= 1;
+                tau[ql] = O[P - 1];
+                cnt[ql] = 0;
+            }
+            __syncwarp();
+        }
+        __syncthreads();
+    }
+    for (int i = threadIdx.x; i < CT_BQ * P; i += 256) {
+        const int ql = i / P, k = i - ql * P;
+        if (q0 + ql < a.nq)
+            a.out[((size_t)blockIdx.x * a.nq + q0 + ql) * P + k] = lists[((size_t)ql * 2 + cur[ql]) * P + k];
+    }
+}
+
+}  // namespace ivfpq

@@ -333,11 +333,44 @@ int set_smem_attr(const void* fn, size_t bytes) {
 cudaStream_t pick_stream(ivfpq_index*, void* stream) { return reinterpret_cast<cudaStream_t>(stream); }
 
 // K1 over the owned centroids: keys [nq, P] (ascending d2, then global id).
+// P <= CT_MAXP: fused exact distance + top-P kernel over centroid slices,
+// slices merged by merge_keys_kernel.  Larger P: distance tiles + block select.
 int run_select(ivfpq_index* idx, const float* d_q, int64_t nq, int64_t P, uint64_t* d_keys, cudaStream_t st) {
     const int64_t nc = idx->nlist_local;
     if (P > MAX_K) return set_err(IVFPQ_EUNSUPPORTED, "nprobe=%lld exceeds the device limit %d", (long long)P, MAX_K);
     if (nc == 0) {
         CK(cudaMemsetAsync(d_keys, 0xff, (size_t)nq * P * 8, st));
+        return IVFPQ_OK;
+    }
+    if (P <= CT_MAXP) {
+        // slices: enough CTAs to fill the GPU twice over, each >= 512 centroids
+        const int64_t qblocks = (nq + CT_BQ - 1) / CT_BQ;
+        int64_t nsl = std::max<int64_t>(1, std::min<int64_t>((2 * idx->num_sms + qblocks - 1) / qblocks, nc / 512));
+        int64_t slice = ((nc + nsl - 1) / nsl + CT_BC - 1) / CT_BC * CT_BC;
+        nsl = (nc + slice - 1) / slice;
+        static bool attr = false;
+        if (!attr) {
+            CKR(set_smem_attr((const void*)coarse_topk_kernel, SMEM_LIMIT - 10 * 1024));
+            attr = true;
+        }
+        uint64_t* out = d_keys;
+        if (nsl > 1) {
+            CKR(idx->dist.ensure((size_t)nsl * nq * P * 8));
+            out = reinterpret_cast<uint64_t*>(idx->dist.p);
+        }
+        CoarseTopkArgs ca{d_q, idx->coarse, idx->l2g, out, (int)nq, (int)nc, (int)idx->d, (int)P, (int)slice};
+        coarse_topk_kernel<<<dim3((unsigned)nsl, (unsigned)qblocks), 256, coarse_topk_smem((int)P), st>>>(ca);
+        KCHECK();
+        if (nsl > 1) {
+            static bool mattr = false;
+            if (!mattr) {
+                CKR(set_smem_attr((const void*)merge_keys_kernel, SMEM_LIMIT));
+                mattr = true;
+            }
+            merge_keys_kernel<<<(unsigned)nq, TK_BLOCK, topk_smem((int)P), st>>>(out, (int)nsl, (int)nq, (int)P, (int)P,
+                                                                               d_keys);
+            KCHECK();
+        }
         return IVFPQ_OK;
     }
     int64_t rows = std::max<int64_t>(1, std::min<int64_t>(nq, (int64_t)(COARSE_CHUNK_BYTES / (nc * 4))));

@@ -314,3 +314,21 @@ def test_many_short_queries_reuse_query_state(pkg, nprobe, k):
         assert np.array_equal(got.ids, want_ids), prec
         assert np.array_equal(got.distances, want_d), prec
         assert n_short == want_short
+
+
+@pytest.mark.parametrize("nprobe", [1, 37, 64, 65, 200])
+def test_select_clusters_fused_and_fallback_paths(pkg, nprobe):
+    """nprobe <= 64 runs the fused distance+top-P kernel over centroid slices,
+    larger nprobe the distance-tile + block-select path; both bit-exact."""
+    from oracle import c_oracle
+    rng = np.random.default_rng(nprobe)
+    idx = _random_index(rng, 20000, 32, 8, 4, 2048)
+    q = rng.random((50, 32)).astype(np.float32)
+    q[1] = idx.coarse[5]                      # exact hit (distance 0)
+    q[2] = (idx.coarse[7] + idx.coarse[9]) / 2  # near-tie
+    for i in range(q.shape[0]):
+        assert np.array_equal(pkg.select_clusters(idx, q[i], nprobe), c_oracle.select(idx.coarse, q[i], nprobe))
+    off, ids, codes = idx.csr()
+    got, _ = pkg.search_batch(idx, q, pkg.SearchParams(k=10, nprobe=nprobe, precision="e5m3"))
+    want_ids, want_d, _ = c_oracle.search_batch(idx.coarse, idx.cb.centers, off, ids, codes, q, 10, nprobe, "e5m3")
+    assert np.array_equal(got.ids, want_ids) and np.array_equal(got.distances, want_d)
