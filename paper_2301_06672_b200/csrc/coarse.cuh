@@ -116,8 +116,9 @@ struct CoarseTopkArgs {
     int nq, nc, d, P, slice;
 };
 
-__host__ __device__ inline size_t coarse_topk_smem(int P) {
-    return (size_t)CT_BQ * (2 * P + CT_BC) * 8 + (size_t)CT_BQ * 16;
+__host__ __device__ inline size_t coarse_topk_smem(int P, int d) {
+    const int dk = (d + CT_BK - 1) / CT_BK * CT_BK;
+    return (size_t)dk * (CT_BQ + 4) * 4 + (size_t)CT_BQ * (2 * P + CT_BC) * 8 + (size_t)CT_BQ * 16;
 }
 
 __device__ __forceinline__ unsigned long long ct_pk2(float a, float b) {
@@ -140,11 +141,12 @@ __device__ __forceinline__ unsigned long long ct_mul2(unsigned long long a, unsi
 }
 
 __global__ void __launch_bounds__(256) coarse_topk_kernel(const CoarseTopkArgs a) {
-    __shared__ __align__(16) float Qs[CT_BK][CT_BQ + 4];
-    __shared__ __align__(16) float Cs[CT_BK][CT_BC + 4];
+    __shared__ __align__(16) float Cs[2][CT_BK][CT_BC + 4];
     extern __shared__ __align__(16) uint8_t ct_smem[];
     const int P = a.P;
-    uint64_t* lists = reinterpret_cast<uint64_t*>(ct_smem);          // [BQ][2][P]
+    const int dk = (a.d + CT_BK - 1) / CT_BK * CT_BK;                  // d padded to the chunk
+    float* Qs = reinterpret_cast<float*>(ct_smem);                     // [dk][BQ + 4], resident
+    uint64_t* lists = reinterpret_cast<uint64_t*>(Qs + (size_t)dk * (CT_BQ + 4));  // [BQ][2][P]
     uint64_t* buf = lists + (size_t)CT_BQ * 2 * P;                     // [BQ][BC]
     int* cnt = reinterpret_cast<int*>(buf + (size_t)CT_BQ * CT_BC);   // [BQ]
     int* cur = cnt + CT_BQ;                                            // [BQ]
@@ -154,11 +156,30 @@ __global__ void __launch_bounds__(256) coarse_topk_kernel(const CoarseTopkArgs a
     const int q0 = blockIdx.y * CT_BQ;
     const int cb = blockIdx.x * a.slice, ce = min(a.nc, cb + a.slice);
     for (int i = threadIdx.x; i < CT_BQ * 2 * P; i += 256) lists[i] = ~0ull;
+    // queries, transposed: Qs[t][q]; zero-padded dims add fl(acc + 0) = acc
+    for (int i = threadIdx.x; i < CT_BQ * dk; i += 256) {
+        const int r = i / dk, t = i - r * dk;
+        Qs[(size_t)t * (CT_BQ + 4) + r] = (q0 + r < a.nq && t < a.d) ? a.Q[(size_t)(q0 + r) * a.d + t] : 0.0f;
+    }
     if (threadIdx.x < CT_BQ) {
         cnt[threadIdx.x] = 0;
         cur[threadIdx.x] = 0;
         tau[threadIdx.x] = ~0ull;
     }
+    // centroid chunk loader: 64 centroids x 16 dims, 4 values per thread
+    const int lr = threadIdx.x >> 2, lk = (threadIdx.x & 3) * 4;  // row, first dim of this thread's 4
+    auto load_chunk = [&](int c0, int k0, float (&v)[4]) {
+        const int cr = c0 + lr;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int kd = k0 + lk + u;
+            v[u] = (cr < ce && kd < a.d) ? __ldg(a.C + (size_t)cr * a.d + kd) : 0.0f;
+        }
+    };
+    const int nchunk = dk / CT_BK;
+    float pre[4];
+    load_chunk(cb, 0, pre);
+    int buf_i = 0;
     __syncthreads();
 
     for (int c0 = cb; c0 < ce; c0 += CT_BC) {
@@ -167,18 +188,18 @@ __global__ void __launch_bounds__(256) coarse_topk_kernel(const CoarseTopkArgs a
         for (int i = 0; i < 4; ++i)
 #pragma unroll
             for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
-        for (int k0 = 0; k0 < a.d; k0 += CT_BK) {
-            for (int i = threadIdx.x; i < CT_BQ * CT_BK; i += 256) {
-                const int r = i / CT_BK, kk = i % CT_BK;
-                const int qr = q0 + r, cr = c0 + r, kd = k0 + kk;
-                Qs[kk][r] = (qr < a.nq && kd < a.d) ? a.Q[(size_t)qr * a.d + kd] : 0.0f;
-                Cs[kk][r] = (cr < ce && kd < a.d) ? a.C[(size_t)cr * a.d + kd] : 0.0f;
-            }
+        for (int kc = 0; kc < nchunk; ++kc) {
+            // publish the prefetched chunk, prefetch the next one (next tile's first at the end)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) Cs[buf_i][lk + u][lr] = pre[u];
+            if (kc + 1 < nchunk) load_chunk(c0, (kc + 1) * CT_BK, pre);
+            else if (c0 + CT_BC < ce) load_chunk(c0 + CT_BC, 0, pre);
             __syncthreads();
+            const float* qb = Qs + (size_t)kc * CT_BK * (CT_BQ + 4);
 #pragma unroll
             for (int kk = 0; kk < CT_BK; ++kk) {
-                const float4 qv = *reinterpret_cast<const float4*>(&Qs[kk][ty * 4]);
-                const float4 cv = *reinterpret_cast<const float4*>(&Cs[kk][tx * 4]);
+                const float4 qv = *reinterpret_cast<const float4*>(qb + kk * (CT_BQ + 4) + ty * 4);
+                const float4 cv = *reinterpret_cast<const float4*>(&Cs[buf_i][kk][tx * 4]);
                 const float qa[4] = {qv.x, qv.y, qv.z, qv.w};
                 const unsigned long long c01 = ct_pk2(cv.x, cv.y), c23 = ct_pk2(cv.z, cv.w);
 #pragma unroll
@@ -194,7 +215,7 @@ __global__ void __launch_bounds__(256) coarse_topk_kernel(const CoarseTopkArgs a
                     acc[i][3] = __fadd_rn(acc[i][3], s3);
                 }
             }
-            __syncthreads();
+            buf_i ^= 1;  // the other buffer is written next chunk; its readers passed this barrier
         }
         // candidates under the query's running P-th key
 #pragma unroll

@@ -342,10 +342,14 @@ int run_select(ivfpq_index* idx, const float* d_q, int64_t nq, int64_t P, uint64
         CK(cudaMemsetAsync(d_keys, 0xff, (size_t)nq * P * 8, st));
         return IVFPQ_OK;
     }
-    if (P <= CT_MAXP) {
-        // slices: enough CTAs to fill the GPU twice over, each >= 512 centroids
+    if (P <= CT_MAXP && coarse_topk_smem((int)P, (int)idx->d) <= SMEM_LIMIT - 24 * 1024) {
+        // slices: ~CT_WAVES CTAs per SM in flight, each slice >= 256 centroids
         const int64_t qblocks = (nq + CT_BQ - 1) / CT_BQ;
-        int64_t nsl = std::max<int64_t>(1, std::min<int64_t>((2 * idx->num_sms + qblocks - 1) / qblocks, nc / 512));
+        static const int waves = [] {
+            const char* e = getenv("IVFPQ_CT_WAVES");
+            return e ? atoi(e) : 6;
+        }();
+        int64_t nsl = std::max<int64_t>(1, std::min<int64_t>((waves * idx->num_sms + qblocks - 1) / qblocks, nc / 256));
         int64_t slice = ((nc + nsl - 1) / nsl + CT_BC - 1) / CT_BC * CT_BC;
         nsl = (nc + slice - 1) / slice;
         static bool attr = false;
@@ -359,7 +363,7 @@ int run_select(ivfpq_index* idx, const float* d_q, int64_t nq, int64_t P, uint64
             out = reinterpret_cast<uint64_t*>(idx->dist.p);
         }
         CoarseTopkArgs ca{d_q, idx->coarse, idx->l2g, out, (int)nq, (int)nc, (int)idx->d, (int)P, (int)slice};
-        coarse_topk_kernel<<<dim3((unsigned)nsl, (unsigned)qblocks), 256, coarse_topk_smem((int)P), st>>>(ca);
+        coarse_topk_kernel<<<dim3((unsigned)nsl, (unsigned)qblocks), 256, coarse_topk_smem((int)P, (int)idx->d), st>>>(ca);
         KCHECK();
         if (nsl > 1) {
             static bool mattr = false;
