@@ -44,6 +44,14 @@ int ivfpq_max_k(void);
  * kernel when the shape fits, else the per-query kernel), 1 = force the
  * per-query kernel. */
 int ivfpq_set_scan_kernel(int mode);
+/* Coarse-select (K1) kernel selection (testing): 0 = auto (tensor-core TF32
+ * nomination + exact re-rank when the shape fits), 1 = exact SIMT kernel only,
+ * 2 = tensor-core path with every query re-done by the exact fallback. */
+int ivfpq_set_select_kernel(int mode);
+/* Debug: number of queries in the last tensor-core coarse select on `idx`
+ * whose error-bound guard failed (and were re-done exactly); -1 if the last
+ * select did not take the tensor-core path.  Synchronises the device. */
+int ivfpq_debug_select_flagged(ivfpq_index *idx, int64_t *out);
 /* Number of CUDA kernels this library has launched since it was loaded. */
 int ivfpq_launch_count(int64_t *out);
 

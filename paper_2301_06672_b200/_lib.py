@@ -30,6 +30,8 @@ SIGNATURES = {
     "ivfpq_max_k": [],
     "ivfpq_launch_count": [_P],
     "ivfpq_set_scan_kernel": [_I32],
+    "ivfpq_set_select_kernel": [_I32],
+    "ivfpq_debug_select_flagged": [_P, _P],
     "ivfpq_index_create": [_I32, _P, _I64, _I64, _P, _I64, _I64, _P, _P, _P, _P, _I64, _P],
     "ivfpq_index_destroy": [_P],
     "ivfpq_index_bytes": [_P, _P],

@@ -114,6 +114,10 @@ struct CoarseTopkArgs {
     const int32_t* l2g;
     uint64_t* out;  // [nslices][nq][P]
     int nq, nc, d, P, slice;
+    // optional indirection (exact re-do of guard failures): row i of this
+    // launch is query qlist[i], i < *qcount; outputs stay at row i
+    const int* qlist = nullptr;
+    const int* qcount = nullptr;
 };
 
 __host__ __device__ inline size_t coarse_topk_smem(int P, int d) {
@@ -153,13 +157,17 @@ __global__ void __launch_bounds__(256) coarse_topk_kernel(const CoarseTopkArgs a
     uint64_t* tau = reinterpret_cast<uint64_t*>(cur + CT_BQ);          // [BQ]
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int q0 = blockIdx.y * CT_BQ;
+    const int nq = a.qcount ? *a.qcount : a.nq;
     const int cb = blockIdx.x * a.slice, ce = min(a.nc, cb + a.slice);
+    // grid-stride over query blocks (one iteration unless the grid was sized
+    // below the query count, as for the tensor-core path's exact re-do)
+    for (int q0 = blockIdx.y * CT_BQ; q0 < nq; q0 += gridDim.y * CT_BQ) {
     for (int i = threadIdx.x; i < CT_BQ * 2 * P; i += 256) lists[i] = ~0ull;
     // queries, transposed: Qs[t][q]; zero-padded dims add fl(acc + 0) = acc
     for (int i = threadIdx.x; i < CT_BQ * dk; i += 256) {
         const int r = i / dk, t = i - r * dk;
-        Qs[(size_t)t * (CT_BQ + 4) + r] = (q0 + r < a.nq && t < a.d) ? a.Q[(size_t)(q0 + r) * a.d + t] : 0.0f;
+        const int qi = q0 + r < nq ? (a.qlist ? a.qlist[q0 + r] : q0 + r) : -1;
+        Qs[(size_t)t * (CT_BQ + 4) + r] = (qi >= 0 && t < a.d) ? a.Q[(size_t)qi * a.d + t] : 0.0f;
     }
     if (threadIdx.x < CT_BQ) {
         cnt[threadIdx.x] = 0;
@@ -273,8 +281,10 @@ __global__ void __launch_bounds__(256) coarse_topk_kernel(const CoarseTopkArgs a
     }
     for (int i = threadIdx.x; i < CT_BQ * P; i += 256) {
         const int ql = i / P, k = i - ql * P;
-        if (q0 + ql < a.nq)
+        if (q0 + ql < nq)
             a.out[((size_t)blockIdx.x * a.nq + q0 + ql) * P + k] = lists[((size_t)ql * 2 + cur[ql]) * P + k];
+    }
+    __syncthreads();
     }
 }
 

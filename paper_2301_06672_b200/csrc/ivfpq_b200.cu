@@ -17,6 +17,7 @@
 #define IVFPQ_DEFINE_PLAN_KERNEL
 #include "codec.cuh"
 #include "coarse.cuh"
+#include "coarse_tc.cuh"
 #include "scan.cuh"
 #include "topk.cuh"
 #include "ws_launch.cuh"
@@ -110,11 +111,14 @@ struct ivfpq_index {
     uint32_t* ids = nullptr;     // [n_local]
     uint8_t* codes = nullptr;    // [n_local * s_pad] interleaved
     float* centers = nullptr;    // [s, 2^p, sub_d]
+    float* tc_img = nullptr;     // K1 tensor-core operand: swizzled centroid tiles (coarse_tc.cuh)
+    float tc_cmax = 0.0f;        // max |c|
+    bool tc_used = false;        // last select took the tensor-core path
     int64_t bytes = 0;
     cudaStream_t stream = nullptr;
     std::mutex mu;
     // scratch
-    DevBuf q, dist, pkeys, oids, odist, oshort, keys, ncand, work, plan_jobs, plan_rq, plan_nj, plan_nc;
+    DevBuf q, dist, pkeys, oids, odist, oshort, keys, ncand, work, plan_jobs, plan_rq, plan_nj, plan_nc, tc_sl, flags;
     int num_sms = 0;
 };
 
@@ -156,25 +160,38 @@ __global__ void interleave_codes_kernel(const uint8_t* __restrict__ src, const i
     }
 }
 
+// qlist/qcount (optional): block b merges row b and writes it to row qlist[b], b < *qcount.
+__global__ void gtimer_kernel(unsigned long long* out) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    *out = t;
+}
+
 __global__ void merge_keys_kernel(const uint64_t* __restrict__ in, int W, int nq, int n_in, int n_out,
-                                  uint64_t* __restrict__ out) {
+                                  uint64_t* __restrict__ out, const int* qlist = nullptr,
+                                  const int* qcount = nullptr) {
     extern __shared__ __align__(16) uint8_t smem[];
-    BlockTopK tk;
-    tk.bind(smem, n_out);
-    tk.init();
-    const int total = W * n_in;
-    for (int base = 0; base < total; base += TK_BLOCK) {
-        const int i = base + threadIdx.x;
-        uint64_t key = ~0ull;
-        if (i < total) {
-            const int w = i / n_in, j = i - w * n_in;
-            key = in[((size_t)w * nq + blockIdx.x) * n_in + j];
+    const int nrows = qcount ? *qcount : nq;
+    for (int row = blockIdx.x; row < nrows; row += gridDim.x) {
+        const int orow = qlist ? qlist[row] : row;
+        BlockTopK tk;
+        tk.bind(smem, n_out);
+        tk.init();
+        const int total = W * n_in;
+        for (int base = 0; base < total; base += TK_BLOCK) {
+            const int i = base + threadIdx.x;
+            uint64_t key = ~0ull;
+            if (i < total) {
+                const int w = i / n_in, j = i - w * n_in;
+                key = in[((size_t)w * nq + row) * n_in + j];
+            }
+            tk.offer(key, key != ~0ull && key < tk.tau());
+            if (base + TK_BLOCK < total) tk.maybe_merge();
         }
-        tk.offer(key, key != ~0ull && key < tk.tau());
-        if (base + TK_BLOCK < total) tk.maybe_merge();
+        tk.merge();
+        for (int i = threadIdx.x; i < n_out; i += TK_BLOCK) out[(size_t)orow * n_out + i] = tk.result()[i];
+        __syncthreads();
     }
-    tk.merge();
-    for (int i = threadIdx.x; i < n_out; i += TK_BLOCK) out[(size_t)blockIdx.x * n_out + i] = tk.result()[i];
 }
 
 __global__ void finalize_kernel(const uint64_t* __restrict__ keys, const int64_t* __restrict__ ncand, int nq, int K,
@@ -332,16 +349,151 @@ int set_smem_attr(const void* fn, size_t bytes) {
 // the CUDA runtime (torch's default stream has handle 0).
 cudaStream_t pick_stream(ivfpq_index*, void* stream) { return reinterpret_cast<cudaStream_t>(stream); }
 
+// 0 = auto (tensor-core K1 when the shape fits), 1 = SIMT only, 2 = tensor
+// core with every query re-done by the exact fallback (tests the fallback);
+// set by ivfpq_set_select_kernel or IVFPQ_SELECT_SIMT=1.
+std::atomic<int> g_select_mode{-1};
+
+int select_mode() {
+    int m = g_select_mode.load();
+    if (m < 0) {
+        const char* e = getenv("IVFPQ_SELECT_SIMT");
+        m = (e && atoi(e) != 0) ? 1 : 0;
+        g_select_mode.store(m);
+    }
+    return m;
+}
+
+int launch_coarse_topk(ivfpq_index* idx, const float* d_q, int64_t nq, int64_t P, int64_t nsl, int64_t slice,
+                       uint64_t* out, const int* qlist, const int* qcount, cudaStream_t st, int64_t max_qblocks = 0) {
+    static bool attr = false;
+    if (!attr) {
+        CKR(set_smem_attr((const void*)coarse_topk_kernel, SMEM_LIMIT - 10 * 1024));
+        attr = true;
+    }
+    CoarseTopkArgs ca{d_q, idx->coarse, idx->l2g, out, (int)nq, (int)idx->nlist_local, (int)idx->d, (int)P, (int)slice};
+    ca.qlist = qlist;
+    ca.qcount = qcount;
+    int64_t qblocks = (nq + CT_BQ - 1) / CT_BQ;
+    if (max_qblocks > 0) qblocks = std::min(qblocks, max_qblocks);
+    coarse_topk_kernel<<<dim3((unsigned)nsl, (unsigned)qblocks), 256, coarse_topk_smem((int)P, (int)idx->d), st>>>(ca);
+    KCHECK();
+    return IVFPQ_OK;
+}
+
+int launch_merge(const uint64_t* in, int64_t W, int64_t nq, int64_t P, uint64_t* out, const int* qlist,
+                 const int* qcount, cudaStream_t st, int64_t max_blocks = 0) {
+    static bool mattr = false;
+    if (!mattr) {
+        CKR(set_smem_attr((const void*)merge_keys_kernel, SMEM_LIMIT));
+        mattr = true;
+    }
+    const int64_t blocks = max_blocks > 0 ? std::min(nq, max_blocks) : nq;
+    merge_keys_kernel<<<(unsigned)blocks, TK_BLOCK, topk_smem((int)P), st>>>(in, (int)W, (int)nq, (int)P, (int)P, out,
+                                                                           qlist, qcount);
+    KCHECK();
+    return IVFPQ_OK;
+}
+
+// Tensor-core K1 (coarse_tc.cuh): TF32 GEMM + shortlist, exact re-rank + guard,
+// exact SIMT re-do of the (rare) queries whose guard failed.
+int run_select_tc(ivfpq_index* idx, const float* d_q, int64_t nq, int64_t P, uint64_t* d_keys, cudaStream_t st) {
+    const int64_t nc = idx->nlist_local, d = idx->d;
+    const int64_t ntiles = (nc + TC_N - 1) / TC_N, nkc = coarse_tc_nkc((int)d);
+    const int64_t qblocks = (nq + TC_M - 1) / TC_M;
+    const int64_t nsl = std::max<int64_t>(1, std::min<int64_t>({(int64_t)TC_MAXSL, ntiles, idx->num_sms / qblocks}));
+    const int64_t tps = (ntiles + nsl - 1) / nsl;
+    const size_t rows = (size_t)nsl * nq;
+    CKR(idx->tc_sl.ensure(rows * TC_CAP * 4 + rows * 8));
+    int32_t* cand = idx->tc_sl.as<int32_t>();
+    int32_t* ncand = cand + rows * TC_CAP;
+    float* thr = reinterpret_cast<float*>(ncand + rows);
+    CKR(idx->flags.ensure((size_t)(nq + 1) * 4));
+    int* fcount = idx->flags.as<int>();
+    int* flist = fcount + 1;
+    CK(cudaMemsetAsync(fcount, 0, sizeof(int), st));
+    idx->tc_used = true;
+    static bool attr = false;
+    if (!attr) {
+        CKR(set_smem_attr((const void*)coarse_tc_kernel, coarse_tc_smem(TC_MAXD)));
+        attr = true;
+    }
+    CoarseTcArgs ta{d_q, idx->tc_img, cand, ncand, thr, (int)nq, (int)nc, (int)d, (int)tps, (int)nkc, 0, nullptr};
+    static const int tc_dbg = [] {
+        const char* e = getenv("IVFPQ_TC_DEBUG");
+        return e ? atoi(e) : 0;
+    }();
+    if (tc_dbg) {
+        static unsigned long long* prof = nullptr;
+        if (!prof) CK(cudaMalloc((void**)&prof, 4096 * 16 * 8));
+        ta.debug = tc_dbg;
+        ta.prof = prof;
+        g_ws_prof = prof;
+    }
+    cudaEvent_t ev[5];
+    const bool timing = (tc_dbg & 8) != 0;
+    if (timing) {
+        for (auto& e : ev) cudaEventCreate(&e);
+        cudaEventRecord(ev[0], st);
+        gtimer_kernel<<<1, 1, 0, st>>>(ta.prof + 4000 * 16);
+    }
+    coarse_tc_kernel<<<dim3((unsigned)nsl, (unsigned)qblocks), TC_THREADS, coarse_tc_smem((int)d), st>>>(ta);
+    if (timing) {
+        gtimer_kernel<<<1, 1, 0, st>>>(ta.prof + 4000 * 16 + 1);
+        cudaEventRecord(ev[1], st);
+    }
+    KCHECK();
+    CoarseRerankArgs ra{d_q, idx->coarse, idx->l2g, cand, ncand, thr, d_keys, fcount, flist, idx->tc_cmax,
+                        (int)nq, (int)nc, (int)d, (int)P, (int)nsl, select_mode() == 2};
+    coarse_rerank_kernel<<<(unsigned)((nq + TC_RR_WARPS - 1) / TC_RR_WARPS), 32 * TC_RR_WARPS,
+                           coarse_rerank_smem((int)nsl, (int)d), st>>>(ra);
+    KCHECK();
+    if (timing) cudaEventRecord(ev[2], st);
+    // exact re-do of flagged queries: grid-stride over the device-side list
+    // (blocks past *fcount exit at once; no host round trip)
+    static bool rattr = false;
+    if (!rattr) {
+        CKR(set_smem_attr((const void*)coarse_redo_kernel, SMEM_LIMIT));
+        rattr = true;
+    }
+    coarse_redo_kernel<<<(unsigned)std::min<int64_t>(nq, 2 * idx->num_sms), TK_BLOCK,
+                         coarse_redo_smem((int)P, (int)d), st>>>(d_q, idx->coarse, idx->l2g, (int)nc, (int)d, (int)P,
+                                                                fcount, flist, d_keys);
+    KCHECK();
+    if (timing) cudaEventRecord(ev[3], st);
+    if (timing) {
+        cudaEventRecord(ev[4], st);
+        cudaEventSynchronize(ev[4]);
+        float ms[4];
+        for (int i = 0; i < 4; ++i) cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1]);
+        unsigned long long gt[2], cs[16];
+        cudaMemcpy(gt, ta.prof + 4000 * 16, 16, cudaMemcpyDeviceToHost);
+        cudaMemcpy(cs, ta.prof, 128, cudaMemcpyDeviceToHost);
+        fprintf(stderr, "marker->cta0 start %.1f us, cta0 end -> marker %.1f us\n", (cs[8] - gt[0]) / 1e3,
+                (gt[1] - cs[9]) / 1e3);
+        fprintf(stderr, "select_tc: tc %.1f us  rerank %.1f us  redo %.1f us  merge %.1f us\n", ms[0] * 1e3,
+                ms[1] * 1e3, ms[2] * 1e3, ms[3] * 1e3);
+        for (auto& e : ev) cudaEventDestroy(e);
+    }
+    return IVFPQ_OK;
+}
+
 // K1 over the owned centroids: keys [nq, P] (ascending d2, then global id).
 // P <= CT_MAXP: fused exact distance + top-P kernel over centroid slices,
 // slices merged by merge_keys_kernel.  Larger P: distance tiles + block select.
 int run_select(ivfpq_index* idx, const float* d_q, int64_t nq, int64_t P, uint64_t* d_keys, cudaStream_t st) {
     const int64_t nc = idx->nlist_local;
     if (P > MAX_K) return set_err(IVFPQ_EUNSUPPORTED, "nprobe=%lld exceeds the device limit %d", (long long)P, MAX_K);
+    if (nq <= 0) return IVFPQ_OK;
     if (nc == 0) {
         CK(cudaMemsetAsync(d_keys, 0xff, (size_t)nq * P * 8, st));
         return IVFPQ_OK;
     }
+    const int smode = select_mode();
+    idx->tc_used = false;
+    if (idx->tc_img && smode != 1 && P <= TC_MAXP && nc >= 2 * TC_N &&
+        coarse_topk_smem((int)P, (int)idx->d) <= SMEM_LIMIT - 24 * 1024)
+        return run_select_tc(idx, d_q, nq, P, d_keys, st);
     if (P <= CT_MAXP && coarse_topk_smem((int)P, (int)idx->d) <= SMEM_LIMIT - 24 * 1024) {
         // slices: ~CT_WAVES CTAs per SM in flight, each slice >= 256 centroids
         const int64_t qblocks = (nq + CT_BQ - 1) / CT_BQ;
@@ -352,29 +504,13 @@ int run_select(ivfpq_index* idx, const float* d_q, int64_t nq, int64_t P, uint64
         int64_t nsl = std::max<int64_t>(1, std::min<int64_t>((waves * idx->num_sms + qblocks - 1) / qblocks, nc / 256));
         int64_t slice = ((nc + nsl - 1) / nsl + CT_BC - 1) / CT_BC * CT_BC;
         nsl = (nc + slice - 1) / slice;
-        static bool attr = false;
-        if (!attr) {
-            CKR(set_smem_attr((const void*)coarse_topk_kernel, SMEM_LIMIT - 10 * 1024));
-            attr = true;
-        }
         uint64_t* out = d_keys;
         if (nsl > 1) {
             CKR(idx->dist.ensure((size_t)nsl * nq * P * 8));
             out = reinterpret_cast<uint64_t*>(idx->dist.p);
         }
-        CoarseTopkArgs ca{d_q, idx->coarse, idx->l2g, out, (int)nq, (int)nc, (int)idx->d, (int)P, (int)slice};
-        coarse_topk_kernel<<<dim3((unsigned)nsl, (unsigned)qblocks), 256, coarse_topk_smem((int)P, (int)idx->d), st>>>(ca);
-        KCHECK();
-        if (nsl > 1) {
-            static bool mattr = false;
-            if (!mattr) {
-                CKR(set_smem_attr((const void*)merge_keys_kernel, SMEM_LIMIT));
-                mattr = true;
-            }
-            merge_keys_kernel<<<(unsigned)nq, TK_BLOCK, topk_smem((int)P), st>>>(out, (int)nsl, (int)nq, (int)P, (int)P,
-                                                                               d_keys);
-            KCHECK();
-        }
+        CKR(launch_coarse_topk(idx, d_q, nq, P, nsl, slice, out, nullptr, nullptr, st));
+        if (nsl > 1) CKR(launch_merge(out, nsl, nq, P, d_keys, nullptr, nullptr, st));
         return IVFPQ_OK;
     }
     int64_t rows = std::max<int64_t>(1, std::min<int64_t>(nq, (int64_t)(COARSE_CHUNK_BYTES / (nc * 4))));
@@ -580,9 +716,30 @@ const char* ivfpq_last_error(void) { return g_err.c_str(); }
 int ivfpq_version(void) { return 1; }
 int ivfpq_max_k(void) { return MAX_K; }
 
+int ivfpq_set_select_kernel(int mode) {
+    if (mode < 0 || mode > 2)
+        return set_err(IVFPQ_EINVAL, "select kernel mode must be 0 (auto), 1 (SIMT) or 2 (tensor core, all re-done)");
+    g_select_mode.store(mode);
+    return IVFPQ_OK;
+}
+
 int ivfpq_set_scan_kernel(int mode) {
     if (mode < 0 || mode > 1) return set_err(IVFPQ_EINVAL, "scan kernel mode must be 0 (auto) or 1 (v1)");
     g_scan_mode.store(mode);
+    return IVFPQ_OK;
+}
+
+// Debug: queries of the last tensor-core K1 on this index whose guard failed
+// (re-done by the exact kernel); -1 if the last select did not use it.
+int ivfpq_debug_select_flagged(ivfpq_index* idx, int64_t* out) {
+    if (!idx || !out) return set_err(IVFPQ_EINVAL, "null argument");
+    DeviceGuard guard(idx->device);
+    int n = -1;
+    if (idx->tc_used) {
+        CK(cudaDeviceSynchronize());
+        CK(cudaMemcpy(&n, idx->flags.p, sizeof(int), cudaMemcpyDeviceToHost));
+    }
+    *out = n;
     return IVFPQ_OK;
 }
 
@@ -712,6 +869,18 @@ int ivfpq_index_create(int device, const float* coarse, int64_t nlist, int64_t d
         g_launches.fetch_add(1, std::memory_order_relaxed);
         CKI(cudaGetLastError());
     }
+    if (nl > 0 && d <= TC_MAXD) {
+        // operand images for the tensor-core K1 (built once per index)
+        const int64_t ntiles = (nl + TC_N - 1) / TC_N, nkc = coarse_tc_nkc((int)d);
+        const size_t ib = (size_t)ntiles * nkc * TC_N * 128;
+        CKI(cudaMalloc((void**)&idx->tc_img, ib));
+        idx->bytes += (int64_t)ib;
+        coarse_tc_prep_kernel<<<(unsigned)ntiles, 256, 0, idx->stream>>>(idx->coarse, (int)nl, (int)d, (int)nkc,
+                                                                         idx->tc_img);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        CKI(cudaGetLastError());
+        idx->tc_cmax = coarse_tc_cmax(hco.data(), nl, d);
+    }
     CKI(cudaStreamSynchronize(idx->stream));
     cudaFree(rowmajor);
 #undef CKI
@@ -723,11 +892,13 @@ int ivfpq_index_destroy(ivfpq_index* idx) {
     if (!idx) return IVFPQ_OK;
     DeviceGuard guard(idx->device);
     if (idx->stream) cudaStreamSynchronize(idx->stream);
-    void* ptrs[] = {idx->coarse, idx->l2g, idx->g2l, idx->glen, idx->off, idx->ids, idx->codes, idx->centers};
+    void* ptrs[] = {idx->coarse, idx->l2g, idx->g2l, idx->glen, idx->off, idx->ids, idx->codes, idx->centers,
+                    idx->tc_img};
     for (void* ptr : ptrs)
         if (ptr) cudaFree(ptr);
     for (DevBuf* b : {&idx->q, &idx->dist, &idx->pkeys, &idx->oids, &idx->odist, &idx->oshort, &idx->keys, &idx->ncand,
-                      &idx->work, &idx->plan_jobs, &idx->plan_rq, &idx->plan_nj, &idx->plan_nc})
+                      &idx->work, &idx->plan_jobs, &idx->plan_rq, &idx->plan_nj, &idx->plan_nc, &idx->tc_sl,
+                      &idx->flags})
         b->release();
     if (idx->stream) cudaStreamDestroy(idx->stream);
     delete idx;

@@ -52,7 +52,8 @@ struct BlockTopK {
         sorted = buf + TK_CAP;
         count = reinterpret_cast<int*>(sorted + TK_CAP);
     }
-    __device__ void init() {
+    __device__ void init() {  // (re)start: empty slot 0 live, no candidates
+        cur = 0;
         for (int i = threadIdx.x; i < K; i += blockDim.x) slots[0][i] = ~0ull;
         if (threadIdx.x == 0) *count = 0;
         __syncthreads();

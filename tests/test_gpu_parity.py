@@ -332,3 +332,85 @@ def test_select_clusters_fused_and_fallback_paths(pkg, nprobe):
     got, _ = pkg.search_batch(idx, q, pkg.SearchParams(k=10, nprobe=nprobe, precision="e5m3"))
     want_ids, want_d, _ = c_oracle.search_batch(idx.coarse, idx.cb.centers, off, ids, codes, q, 10, nprobe, "e5m3")
     assert np.array_equal(got.ids, want_ids) and np.array_equal(got.distances, want_d)
+
+
+def _select_batch(pkg, dev, q, nprobe):
+    import torch
+    from paper_2301_06672_b200 import _lib
+    qt = torch.from_numpy(np.ascontiguousarray(q)).cuda()
+    out = torch.empty((q.shape[0], nprobe), dtype=torch.int64, device="cuda")
+    _lib.check(_lib.lib.ivfpq_select_device(dev.handle, qt.data_ptr(), q.shape[0], nprobe, out.data_ptr(),
+                                            torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    keys = out.cpu().numpy().view(np.uint64)
+    return (keys & np.uint64(0xffffffff)).astype(np.int64), (keys >> np.uint64(32)).astype(np.uint32).view(np.float32)
+
+
+def _flagged(dev):
+    from paper_2301_06672_b200 import _lib
+    n = _lib.ctypes.c_int64()
+    _lib.check(_lib.lib.ivfpq_debug_select_flagged(dev.handle, _lib.ctypes.byref(n)))
+    return n.value
+
+
+@pytest.fixture(params=["auto", "simt", "tc_all_fallback"])
+def select_mode(request, pkg):
+    from paper_2301_06672_b200 import _lib
+    _lib.check(_lib.lib.ivfpq_set_select_kernel({"auto": 0, "simt": 1, "tc_all_fallback": 2}[request.param]))
+    yield request.param
+    _lib.check(_lib.lib.ivfpq_set_select_kernel(0))
+
+
+@pytest.mark.parametrize("nlist,d,nq,P", [
+    (4096, 128, 300, 32),    # cfg2 shape: tensor-core nomination + exact re-rank
+    (1000, 96, 131, 8),      # partial centroid tile and query block
+    (2048, 100, 257, 1),     # d not a multiple of 4 / of the 32-wide K chunk
+    (700, 160, 64, 17),      # largest d with resident queries
+    (4096, 128, 40, 32),     # few query blocks -> several centroid slices merged
+])
+def test_select_tensor_core_path_bit_exact(pkg, select_mode, nlist, d, nq, P):
+    """K1 on tcgen05 (TF32 nomination, exact re-rank, guard, exact re-do of
+    flagged queries) returns the reference's probes and distances bit for bit;
+    includes duplicated centroids (exact ties -> smaller id) and queries that
+    sit on a centroid."""
+    from oracle import c_oracle
+    from paper_2301_06672_b200.index import DeviceIndex
+    rng = np.random.default_rng(nlist + d + nq)
+    idx = _random_index(rng, 4 * nlist, d, d // 4 if d % 4 == 0 else d // 2, 4, nlist)
+    idx.coarse[10] = idx.coarse[3]        # exact duplicate centroids
+    idx.coarse[nlist - 1] = idx.coarse[3]
+    q = rng.random((nq, d)).astype(np.float32)
+    q[0] = idx.coarse[3]
+    q[1] = idx.coarse[nlist // 2] + 1e-7
+    dev = DeviceIndex(idx, 0)
+    got, got_d = _select_batch(pkg, dev, q, P)
+    flagged = _flagged(dev)
+    if select_mode == "auto":      # the tensor cores did the nominating, the re-do is rare
+        assert 0 <= flagged <= max(2, nq // 50), flagged
+    elif select_mode == "tc_all_fallback":
+        assert flagged == nq
+    else:
+        assert flagged == -1
+    for i in range(nq):
+        want = c_oracle.select(idx.coarse, q[i], P)
+        assert np.array_equal(got[i], want), (select_mode, i)
+        wd = ((idx.coarse[want] - q[i]) ** 2).astype(np.float32)
+        acc = np.zeros(P, np.float32)
+        for t in range(d):
+            acc = (acc + wd[:, t]).astype(np.float32)
+        assert np.array_equal(got_d[i], acc), (select_mode, i)
+
+
+def test_select_tensor_core_owned_shard(pkg, select_mode):
+    """A list shard (owned subset, local -> global ids) through the tensor-core K1."""
+    from oracle import c_oracle
+    from paper_2301_06672_b200.index import DeviceIndex
+    rng = np.random.default_rng(7)
+    idx = _random_index(rng, 8000, 64, 16, 4, 1024)
+    owned = np.sort(rng.choice(1024, 600, replace=False)).astype(np.int32)
+    q = rng.random((200, 64)).astype(np.float32)
+    dev = DeviceIndex(idx, 0, owned=owned)
+    got, _ = _select_batch(pkg, dev, q, 16)
+    for i in range(q.shape[0]):
+        local = c_oracle.select(idx.coarse[owned], q[i], 16)
+        assert np.array_equal(got[i], owned[local].astype(np.int64)), i
