@@ -63,7 +63,8 @@ def dump_prof(nsm=148):
     fn.argtypes = [ctypes.c_void_p, ctypes.c_int64]
     _lib.check(fn(buf.ctypes.data, buf.nbytes))
     b = buf.astype(np.float64) / 1e6
-    roles = {"builders": range(0, 16), "scanners": range(16, 31), "prep": [31]}
+    bw, sw = int(os.environ.get("WS_BW", "8")), int(os.environ.get("WS_SW", "11"))  # WS_BW_CFG / WS_SW_CFG
+    roles = {"builders": range(0, bw), "scanners": range(bw, bw + sw), "prep": [bw + sw]}
     for name, ws in roles.items():
         m = b[:, list(ws), :].mean(axis=(0, 1))
         print(f"  {name:9s} Mcycles/warp: " + " ".join(f"{x:7.3f}" for x in m))

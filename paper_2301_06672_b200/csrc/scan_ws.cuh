@@ -128,6 +128,14 @@ __device__ __forceinline__ u64 add2(u64 a, u64 b) {
         : "l"(a), "l"(b));
     return r;
 }
+// Packed add of two independent sums: (acc.x + x.x, acc.y + x.y), each one
+// fl(acc + x).  Only for addends that are not multiply results (LUT values),
+// so there is nothing for ptxas to contract.
+__device__ __forceinline__ u64 addx2(u64 a, u64 b) {
+    u64 r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
 __device__ __forceinline__ u64 mulrzftz2(u64 a, u64 b) {
     u64 r;
     asm("mul.rz.ftz.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
@@ -153,15 +161,41 @@ __device__ __forceinline__ void mbar_arrive(u64* bar) {
                      (uint32_t)__cvta_generic_to_shared(bar))
                  : "memory");
 }
+// Critical-path wait (builders / scanners): try_wait with a suspend-time
+// hint -- the warp parks in NANOSLEEP.SYNCS and is woken by barrier traffic
+// (measured faster than a plain spin or a timed backoff here).
+#ifndef WS_WAIT_HINT_NS
+#define WS_WAIT_HINT_NS 1000000
+#endif
 __device__ __forceinline__ void mbar_wait(u64* bar, uint32_t parity) {
     const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
         "@!p bra WAIT_%=;\n\t}" ::"r"(a),
-        "r"(parity)
+        "r"(parity), "n"(WS_WAIT_HINT_NS)
         : "memory");
+}
+__device__ __forceinline__ bool mbar_try(u64* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"((uint32_t)__cvta_generic_to_shared(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+// Wait of a role that is normally ahead (prep warp, builders waiting for a
+// free LUT slot): exponential nanosleep backoff, so the waiting warp does
+// not take issue slots from the builders/scanners sharing its SMSP.
+template <int MAX_NS>
+__device__ __forceinline__ void mbar_wait_backoff(u64* bar, uint32_t parity) {
+    unsigned ns = 32;
+    while (!mbar_try(bar, parity)) {
+        __nanosleep(ns);
+        ns = ns * 2 > (unsigned)MAX_NS ? (unsigned)MAX_NS : ns * 2;
+    }
 }
 __device__ __forceinline__ void mbar_expect_tx(u64* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr_(bar)), "r"(bytes) : "memory");
@@ -549,6 +583,41 @@ __device__ __forceinline__ float ws_acc16(float acc, uint4 w, uint32_t base, int
     return acc;
 }
 
+// Two vectors per lane (consecutive blocks of the warp, possibly of two lists
+// with LUT bases ba / bb): the two sequential sums advance together in one
+// packed add per code -- 3.5 instructions per lookup instead of 4, and two
+// independent dependency chains.
+template <int DT, int LOGN, int B>
+__device__ __forceinline__ u64 ws_acc1x2(u64 acc, uint4 wa, uint4 wb, uint32_t ba, uint32_t bb, int nvalid,
+                                         bool full) {
+    const uint32_t xa = B < 4 ? wa.x : B < 8 ? wa.y : B < 12 ? wa.z : wa.w;
+    const uint32_t xb = B < 4 ? wb.x : B < 8 ? wb.y : B < 12 ? wb.z : wb.w;
+    if (full || B < nvalid) acc = addx2(acc, pk2(ws_gather<DT, LOGN, B>(xa, ba), ws_gather<DT, LOGN, B>(xb, bb)));
+    return acc;
+}
+
+template <int DT, int LOGN>
+__device__ __forceinline__ u64 ws_acc16x2(u64 acc, uint4 wa, uint4 wb, uint32_t ba, uint32_t bb, int nvalid,
+                                          bool full) {
+    acc = ws_acc1x2<DT, LOGN, 0>(acc, wa, wb, ba, bb, nvalid, full);
+    acc = ws_acc1x2<DT, LOGN, 1>(acc, wa, wb, ba, bb, nvalid, full);
+    acc = ws_acc1x2<DT, LOGN, 2>(acc, wa, wb, ba, bb, nvalid, full);
+    acc = ws_acc1x2<DT, LOGN, 3>(acc, wa, wb, ba, bb, nvalid, full);
+    acc = ws_acc1x2<DT, LOGN, 4>(acc, wa, wb, ba, bb, nvalid, full);
+    acc = ws_acc1x2<DT, LOGN, 5>(acc, wa, wb, ba, bb, nvalid, full);
+    acc = ws_acc1x2<DT, LOGN, 6>(acc, wa, wb, ba, bb, nvalid, full);
+    acc = ws_acc1x2<DT, LOGN, 7>(acc, wa, wb, ba, bb, nvalid, full);
+    acc = ws_acc1x2<DT, LOGN, 8>(acc, wa, wb, ba, bb, nvalid, full);
+    acc = ws_acc1x2<DT, LOGN, 9>(acc, wa, wb, ba, bb, nvalid, full);
+    acc = ws_acc1x2<DT, LOGN, 10>(acc, wa, wb, ba, bb, nvalid, full);
+    acc = ws_acc1x2<DT, LOGN, 11>(acc, wa, wb, ba, bb, nvalid, full);
+    acc = ws_acc1x2<DT, LOGN, 12>(acc, wa, wb, ba, bb, nvalid, full);
+    acc = ws_acc1x2<DT, LOGN, 13>(acc, wa, wb, ba, bb, nvalid, full);
+    acc = ws_acc1x2<DT, LOGN, 14>(acc, wa, wb, ba, bb, nvalid, full);
+    acc = ws_acc1x2<DT, LOGN, 15>(acc, wa, wb, ba, bb, nvalid, full);
+    return acc;
+}
+
 // Block table of one job for one scanner warp, held lane-parallel: lane l
 // describes the warp's block k0 + l (job block b = sw + (k0 + l) * SW), i.e.
 // pair g and vectors [vo, vo + nb) of that pair's list.  Built once per job
@@ -662,55 +731,89 @@ __device__ __forceinline__ void ws_scan_job(const ScanArgs& a, const WsJob* J, c
     WsTab ct;
     ct.load(J, sw, lane, 0);
     long long _p0 = 0;
-    for (int k = 0; k < ct.n; ++k) {
-        if (k - ct.k0 >= 32) ct.load(J, sw, lane, k);
+    for (int k = 0; k < ct.n;) {
+        const bool two = k + 1 < ct.n;  // warp-uniform
+        if (k + (two ? 1 : 0) - ct.k0 >= 32) ct.load(J, sw, lane, k);
         {
             WS_P0();
             sg.top_up(a, jobs, full, cjob, lane);
             WS_PA(3);
         }
         WS_P0();
-        int g, nb;
-        long long vo;
-        ct.get(k, g, nb, vo);
-        // the id is fetched up front; the table lookups below hide its latency
-        const uint32_t id = lane < nb ? (a.debug_skip_ids ? (uint32_t)(vo + lane) : __ldg(a.ids + vo + lane)) : 0u;
-        const int st = sg.cs;
+        int g0, nb0, g1 = 0, nb1 = 0;
+        long long vo0, vo1 = 0;
+        ct.get(k, g0, nb0, vo0);
+        if (two) ct.get(k + 1, g1, nb1, vo1);
+        // ids are fetched up front; the table lookups below hide their latency
+        const uint32_t id0 =
+            lane < nb0 ? (a.debug_skip_ids ? (uint32_t)(vo0 + lane) : __ldg(a.ids + vo0 + lane)) : 0u;
+        const uint32_t id1 =
+            lane < nb1 ? (a.debug_skip_ids ? (uint32_t)(vo1 + lane) : __ldg(a.ids + vo1 + lane)) : 0u;
+        const int st0 = sg.cs;
+        const int st1 = st0 + 1 == sg.SD ? 0 : st0 + 1;
+        const uint32_t ph1 = st0 + 1 == sg.SD ? (uint32_t)(sg.cph ^ 1) : (uint32_t)sg.cph;
         WS_PA(4);
         {
             WS_P0();
-            if (!a.debug_skip_copy) mbar_wait(sg.sbar + st, sg.cph);
+            if (!a.debug_skip_copy) {
+                mbar_wait(sg.sbar + st0, sg.cph);
+                if (two) mbar_wait(sg.sbar + st1, ph1);
+            }
             WS_PA(5);
         }
         WS_P0();
-        const uint32_t src = sg.stage0 + st * sg.stage_bytes + lane * 16, cstride = (uint32_t)nb * 16;
-        const uint32_t base = lut_s + g * lut_each;
-        float acc = 0.f;
-        int c = a.debug_skip_gather ? nch : 0;  // debug bit 1
-        for (; c + 2 <= nfull; c += 2) {
-            const uint4 w0 = lds128(src + c * cstride), w1 = lds128(src + (c + 1) * cstride);
-            acc = ws_acc16<DT, LOGN>(acc, w0, base + (uint32_t)(c * 16 * N * E), 16, true);
-            acc = ws_acc16<DT, LOGN>(acc, w1, base + (uint32_t)((c + 1) * 16 * N * E), 16, true);
-        }
-        for (; c < nch; ++c) {
-            const uint4 w0 = lds128(src + c * cstride);
-            acc = ws_acc16<DT, LOGN>(acc, w0, base + (uint32_t)(c * 16 * N * E), a.s - 16 * c, c < nfull);
+        const uint32_t src0 = sg.stage0 + st0 * sg.stage_bytes + lane * 16, cs0 = (uint32_t)nb0 * 16;
+        const uint32_t base0 = lut_s + g0 * lut_each;
+        float acc0 = 0.f, acc1 = 0.f;
+        if (two) {
+            const uint32_t src1 = sg.stage0 + st1 * sg.stage_bytes + lane * 16, cs1 = (uint32_t)nb1 * 16;
+            const uint32_t base1 = lut_s + g1 * lut_each;
+            u64 acc = pk2(0.f, 0.f);
+            int c = a.debug_skip_gather ? nch : 0;  // debug bit 1
+            for (; c < nfull; ++c) {
+                const uint4 wa = lds128(src0 + c * cs0), wb = lds128(src1 + c * cs1);
+                const uint32_t o = (uint32_t)(c * 16 * N * E);
+                acc = ws_acc16x2<DT, LOGN>(acc, wa, wb, base0 + o, base1 + o, 16, true);
+            }
+            for (; c < nch; ++c) {
+                const uint4 wa = lds128(src0 + c * cs0), wb = lds128(src1 + c * cs1);
+                const uint32_t o = (uint32_t)(c * 16 * N * E);
+                acc = ws_acc16x2<DT, LOGN>(acc, wa, wb, base0 + o, base1 + o, a.s - 16 * c, false);
+            }
+            upk2(acc, acc0, acc1);
+        } else {
+            int c = a.debug_skip_gather ? nch : 0;  // debug bit 1
+            for (; c + 2 <= nfull; c += 2) {
+                const uint4 w0 = lds128(src0 + c * cs0), w1 = lds128(src0 + (c + 1) * cs0);
+                acc0 = ws_acc16<DT, LOGN>(acc0, w0, base0 + (uint32_t)(c * 16 * N * E), 16, true);
+                acc0 = ws_acc16<DT, LOGN>(acc0, w1, base0 + (uint32_t)((c + 1) * 16 * N * E), 16, true);
+            }
+            for (; c < nch; ++c) {
+                const uint4 w0 = lds128(src0 + c * cs0);
+                acc0 = ws_acc16<DT, LOGN>(acc0, w0, base0 + (uint32_t)(c * 16 * N * E), a.s - 16 * c, c < nfull);
+            }
         }
         __syncwarp();
         WS_PA(6);
         WS_P0();
-        ++sg.consumed;
-        if (++sg.cs == sg.SD) {
-            sg.cs = 0;
+        const int used = two ? 2 : 1;
+        sg.consumed += used;
+        sg.cs += used;
+        if (sg.cs >= sg.SD) {
+            sg.cs -= sg.SD;
             sg.cph ^= 1;
         }
-        const uint32_t rb = __float_as_uint(lut_finish<DT>(acc));
         const u64 tau = *(volatile u64*)&S->tau;
-        const u64 key = ((u64)rb << 32) | id;
-        const bool pass = lane < nb && key < tau && !a.debug_skip_gather;
-        tk.offer(key, pass);
+        const u64 key0 = ((u64)__float_as_uint(lut_finish<DT>(acc0)) << 32) | id0;
+        tk.offer(key0, lane < nb0 && key0 < tau && !a.debug_skip_gather);
         if (tk.n > WS_WBUF - 32) tk.flush(S, qlist, K);
+        if (two) {
+            const u64 key1 = ((u64)__float_as_uint(lut_finish<DT>(acc1)) << 32) | id1;
+            tk.offer(key1, lane < nb1 && key1 < tau && !a.debug_skip_gather);
+            if (tk.n > WS_WBUF - 32) tk.flush(S, qlist, K);
+        }
         WS_PA(7);
+        k += used;
     }
     sg.top_up(a, jobs, full, cjob, lane);  // keep the ring busy into the next job(s)
 #undef WS_P0
