@@ -566,13 +566,32 @@ bool ws_plan(const ivfpq_index* idx, int64_t P, int64_t K, int dt, WsPlan* plan)
                                      2, (int)K, 2, (int)idx->s_pad).lut_each;
     int G = (int)std::max<size_t>(1, std::min<size_t>(WS_MAX_G, lut_budget_bytes() / lut_each));
     G = (int)std::min<int64_t>(G, std::max<int64_t>(1, P));
-    for (; G >= 1; --G)
-        for (int sd = WS_MAX_SD; sd >= 2; --sd)
-            for (int nb = WS_MAX_NBUF; nb >= 2; --nb) {
+    static const int env_sd = [] {
+        const char* e = getenv("IVFPQ_WS_SD");
+        return e ? atoi(e) : 0;
+    }();
+    static const int env_nb = [] {
+        const char* e = getenv("IVFPQ_WS_NBUF");
+        return e ? atoi(e) : 0;
+    }();
+    // Preference (measured on cfg2): >= 3 LUT slots (builders and scanners
+    // decoupled by a job of slack) with the largest G >= 2 that allows them
+    // (fp8: G=3 x 3 slots, 4.86 ms vs G=4 x 2 slots, 5.18 ms), then code
+    // stages; otherwise 2 slots (f16: G=2 x 2, 6.33 ms vs G=1 x 4, 7.38 ms).
+    const int G0 = G;
+    for (int min_nb = 3; min_nb >= 2; --min_nb)
+    for (G = G0; G >= (min_nb == 3 ? 2 : 1); --G)
+        for (int sd = env_sd ? env_sd : WS_MAX_SD; sd >= 2; --sd)
+            for (int nb = env_nb ? env_nb : WS_MAX_NBUF; nb >= min_nb; --nb) {
                 const size_t sm = WsLayout((int)idx->d, (int)idx->s, (int)idx->sub_d, (int)idx->p, lut_bytes_of((int)dt),
                                            G, nb, (int)K, sd, (int)idx->s_pad).total;
                 if (sm <= SMEM_LIMIT) {
                     *plan = WsPlan{G, nb, sd, sm};
+                    static bool printed = false;
+                    if (!printed && getenv("IVFPQ_WS_PLAN_PRINT")) {
+                        fprintf(stderr, "scan_ws plan: G=%d NBUF=%d SD=%d smem=%zu\n", G, nb, sd, sm);
+                        printed = true;
+                    }
                     return true;
                 }
             }

@@ -384,8 +384,31 @@ struct WsBuild {
         constexpr int E = sizeof(T);
         const uint32_t rqb = rq_s + (uint32_t)jr * SUB_D * 4;
         const uint32_t lb = lut_s + ((uint32_t)jr * N + 4 * u) * E;
+        // two owned rows per iteration: 2 x ng independent entry chains in flight
+        int i = 0;
 #pragma unroll 1
-        for (int i = 0; i < jpt; ++i) {
+        for (; i + 2 <= jpt; i += 2) {
+            uint32_t c0[CPI], c1[CPI];
+            tmem_ld<CPI>(tbase + i * CPI, c0);
+            tmem_ld<CPI>(tbase + (i + 1) * CPI, c1);
+            tmem_wait_ld();
+            u64 cenA[2][SUB_D], cenB[2][SUB_D];
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int x = 0; x < SUB_D; ++x) {
+                    cenA[h][x] = pk2(__uint_as_float(c0[(h * SUB_D + x) * 2]), __uint_as_float(c0[(h * SUB_D + x) * 2 + 1]));
+                    cenB[h][x] = pk2(__uint_as_float(c1[(h * SUB_D + x) * 2]), __uint_as_float(c1[(h * SUB_D + x) * 2 + 1]));
+                }
+            const uint32_t raA = rqb + i * R * SUB_D * 4, laA = lb + i * R * N * E;
+            const uint32_t raB = raA + R * SUB_D * 4, laB = laA + R * N * E;
+#pragma unroll 2
+            for (int g = 0; g < ng; ++g) {
+                entry_quad(cenA, raA + g * rq_stride, laA + g * lut_stride);
+                entry_quad(cenB, raB + g * rq_stride, laB + g * lut_stride);
+            }
+        }
+        if (i < jpt) {
             uint32_t c[CPI];
             tmem_ld<CPI>(tbase + i * CPI, c);
             tmem_wait_ld();
@@ -397,30 +420,33 @@ struct WsBuild {
                     cen[h][x] = pk2(__uint_as_float(c[(h * SUB_D + x) * 2]), __uint_as_float(c[(h * SUB_D + x) * 2 + 1]));
             const uint32_t ra0 = rqb + i * R * SUB_D * 4, la0 = lb + i * R * N * E;
 #pragma unroll 4
-            for (int g = 0; g < ng; ++g) {
-                float r[SUB_D];
-                const uint32_t ra = ra0 + g * rq_stride;
-                if constexpr (SUB_D == 2) {
-                    lds_f32x2(ra, r[0], r[1]);
-                } else if constexpr (SUB_D == 4) {
-                    lds_f32x4(ra, r[0], r[1], r[2], r[3]);
-                } else {
-#pragma unroll
-                    for (int x = 0; x < SUB_D; ++x) r[x] = lds_f32(ra + 4 * x);
-                }
-                u64 acc0 = 0, acc1 = 0;
-#pragma unroll
-                for (int x = 0; x < SUB_D; ++x) {
-                    const u64 rr = pk2(r[x], r[x]);
-                    const u64 d0 = sub2(cen[0][x], rr), d1 = sub2(cen[1][x], rr);
-                    const u64 q0 = mul2(d0, d0), q1 = mul2(d1, d1);
-                    // acc starts at +0: fl(0 + q) = q exactly (q >= +0)
-                    acc0 = x == 0 ? q0 : add2(acc0, q0);
-                    acc1 = x == 0 ? q1 : add2(acc1, q1);
-                }
-                store(la0 + g * lut_stride, acc0, acc1);
-            }
+            for (int g = 0; g < ng; ++g) entry_quad(cen, ra0 + g * rq_stride, la0 + g * lut_stride);
         }
+    }
+
+    // Four LUT entries (codes 4u..4u+3 of one subspace row) for one list:
+    // T = seq_x fl(acc + fl(fl(c - rq)^2)), then the storage encode.
+    __device__ __forceinline__ static void entry_quad(const u64 (&cen)[2][SUB_D], uint32_t ra, uint32_t dst) {
+        float r[SUB_D];
+        if constexpr (SUB_D == 2) {
+            lds_f32x2(ra, r[0], r[1]);
+        } else if constexpr (SUB_D == 4) {
+            lds_f32x4(ra, r[0], r[1], r[2], r[3]);
+        } else {
+#pragma unroll
+            for (int x = 0; x < SUB_D; ++x) r[x] = lds_f32(ra + 4 * x);
+        }
+        u64 acc0 = 0, acc1 = 0;
+#pragma unroll
+        for (int x = 0; x < SUB_D; ++x) {
+            const u64 rr = pk2(r[x], r[x]);
+            const u64 d0 = sub2(cen[0][x], rr), d1 = sub2(cen[1][x], rr);
+            const u64 q0 = mul2(d0, d0), q1 = mul2(d1, d1);
+            // acc starts at +0: fl(0 + q) = q exactly (q >= +0)
+            acc0 = x == 0 ? q0 : add2(acc0, q0);
+            acc1 = x == 0 ? q1 : add2(acc1, q1);
+        }
+        store(dst, acc0, acc1);
     }
 
     __device__ __forceinline__ static void store(uint32_t dst, u64 a01, u64 a23) {
