@@ -19,7 +19,6 @@ from __future__ import annotations
 import argparse
 import json
 import os
-import subprocess
 import sys
 import tempfile
 import time
@@ -39,7 +38,7 @@ THROTTLE_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_p
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="cfg2")
@@ -58,37 +57,57 @@ def log(*a):
 
 # ------------------------------------------------------------------ clocks ----
 class Clocks:
+    """SM clock + clock-event reasons sampled DURING the timed region by an
+    NVML thread (~1 kHz; the timed region is tens of ms, far below
+    nvidia-smi's 200 ms polling period).  Idle samples are dropped."""
+
     def __init__(self):
-        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
-        q = "clocks.sm,clocks.max.sm,clocks_event_reasons.active"
+        import threading
+        self.rows = []
+        self.stop_ev = threading.Event()
         try:
-            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms",
-                                       "200", "-i", os.environ.get("LOCAL_RANK", "0")], stdout=self.f,
-                                      stderr=subprocess.DEVNULL)
-        except FileNotFoundError:
-            self.p = None
+            import pynvml
+            pynvml.nvmlInit()
+            idx = int(os.environ.get("LOCAL_RANK", "0"))
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            if vis and vis.split(",")[idx].strip().isdigit():
+                idx = int(vis.split(",")[idx])
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # noqa: BLE001 -- no NVML: report null clocks
+            log(f"[bench] NVML unavailable: {e}")
+            self.nv = None
+            return
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+
+    def _run(self):
+        nv, h = self.nv, self.h
+        while not self.stop_ev.is_set():
+            try:
+                self.rows.append((nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM),
+                                  nv.nvmlDeviceGetCurrentClocksEventReasons(h)))
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.001)
 
     def stop(self):
-        if self.p is None:
+        if self.nv is None:
             return None
-        self.p.terminate()
-        self.p.wait()
-        rows = []
-        for line in open(self.f.name):
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) == 3 and parts[0].isdigit():
-                rows.append((int(parts[0]), int(parts[1]), int(parts[2], 16)))
-        os.unlink(self.f.name)
+        self.stop_ev.set()
+        self.t.join()
+        rows = self.rows
         if not rows:
             return None
-        busy = [r for r in rows if not (r[2] & 0x1)] or rows
+        busy = [r for r in rows if not (r[1] & 0x1)] or rows
         reasons = set()
         for r in busy:
             for bit, name in THROTTLE_BITS.items():
-                if r[2] & bit and bit != 0x1:
+                if r[1] & bit and bit != 0x1:
                     reasons.add(name)
-        return {"sm_mhz": float(np.median([r[0] for r in busy])), "sm_max_mhz": max(r[1] for r in rows),
-                "reasons": sorted(reasons), "samples": len(rows)}
+        return {"sm_mhz": float(np.median([r[0] for r in busy])), "sm_max_mhz": int(self.max_mhz),
+                "reasons": sorted(reasons), "samples": len(rows), "busy_samples": len(busy), "source": "nvml"}
 
 
 # ---------------------------------------------------------------- workload ----
@@ -349,7 +368,7 @@ def roofline(srch, idx, q_dev, k, P, prec, flush, torch):
         traffic = tr.get(prec)
     except (OSError, ValueError):
         pass
-    return {"bound": "hbm", "kernel": f"scan_kernel<{prec}> (K2 LUT build + K3 scan + K4 top-k)",
+    return {"bound": "hbm", "kernel": f"scan_ws_kernel<{prec}> (K2 LUT build + K3 scan + K4 top-k)",
             "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
             "traffic": traffic, "algorithmic_bytes_per_launch": int(B), "scan_ms": round(float(t_scan), 4),
             "select_ms": round(float(t_sel), 4),

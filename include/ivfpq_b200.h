@@ -115,6 +115,23 @@ int ivfpq_select_clusters(ivfpq_index *idx, const float *q, int64_t nq, int64_t 
 /* search.py:145-155 top_k: out arrays hold min(n, k) entries */
 int ivfpq_top_k(const int64_t *ids, const float *dists, int64_t n, int64_t k, int64_t *out_ids, float *out_dists);
 
+/* --- ingest: populate an index on the GPU ----------- */
+/* pq_encode (pq.py:92-110): nearest sub-centroid per subspace, ties -> lower
+ * code, BIT-EXACT with the reference (its sgemm FMA chain + einsum norms,
+ * ingest.cuh) for sub_d = d/s <= 4.  x f32[n,d] row-major; codes u8[n,s].
+ * With d_coarse and d_assign (i64[n]) the residual rows fl(x - coarse[a])
+ * of compute_residuals (pq.py:54-63) are formed on the fly. */
+int ivfpq_pq_encode_device(const float *d_x, int64_t n, int64_t d, const float *d_coarse, const int64_t *d_assign,
+                           const float *d_centers, int64_t s, int64_t p, uint8_t *d_codes, void *stream);
+int ivfpq_pq_encode(const float *x, int64_t n, int64_t d, const float *centers, int64_t s, int64_t p,
+                    uint8_t *codes);
+/* assign_to_centroids (kmeans.py:49-69): nearest centroid under the expanded
+ * squared L2 form clipped at 0, ties -> lower id; d2 may be NULL.  Parity is
+ * decision-level (einsum's norm order at d >= 16 is not modelled). */
+int ivfpq_assign_device(const float *d_x, int64_t n, int64_t d, const float *d_c, int64_t nc, int64_t *d_assign,
+                        float *d_d2, void *stream);
+int ivfpq_assign(const float *x, int64_t n, int64_t d, const float *c, int64_t nc, int64_t *assign, float *d2);
+
 #ifdef __cplusplus
 }
 #endif

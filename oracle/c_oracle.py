@@ -39,6 +39,7 @@ def lib():
         L.orc_build_lut.argtypes = [P, i32, i32, i32, P, i32, P]
         L.orc_scan.argtypes = [P, i64, i32, i32, P, i32, P]
         L.orc_brute_force_knn.argtypes = [P, i64, i32, P, i32, i32, P, P, i32]
+        L.orc_pq_encode.argtypes = [P, i64, i32, P, i32, i32, P]
         L.orc_fp8_encode.restype = ctypes.c_uint8
         L.orc_fp8_encode.argtypes = [ctypes.c_float, i32]
         L.orc_f16_encode.restype = ctypes.c_uint16
@@ -114,3 +115,15 @@ def brute_force_knn(base, queries, k, threads=None):
     lib().orc_brute_force_knn(_p(base), base.shape[0], base.shape[1], _p(queries), nq, k,
                               _p(out_ids), _p(out_d), threads or os.cpu_count() or 1)
     return out_ids, out_d
+
+
+def pq_encode(residuals: np.ndarray, centers: np.ndarray) -> np.ndarray:
+    """pq.py:92-110 restated (sub_d <= 4): codes uint8[n, s]."""
+    X = np.ascontiguousarray(residuals, dtype=np.float32)
+    C = np.ascontiguousarray(centers, dtype=np.float32)
+    s, n_codes, sub = C.shape
+    out = np.empty((X.shape[0], s), dtype=np.uint8)
+    rc = lib().orc_pq_encode(_p(X), X.shape[0], X.shape[1], _p(C), s, n_codes, _p(out))
+    if rc != 0:
+        raise ValueError("oracle pq_encode supports sub_d <= 4 only")
+    return out

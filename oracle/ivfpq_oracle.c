@@ -188,3 +188,57 @@ void orc_brute_force_knn(const float *base, int64_t n, int d, const float *queri
         free(d2); free(c);
     }
 }
+
+/* ---- ingest: pq_encode (pq.py:92-110) via assign_to_centroids (kmeans.py:49-69)
+ * per subspace, restating the BLAS / einsum arithmetic numpy uses for it
+ * (probed in the build container, pinned by tests/golden/pq_encode.npz):
+ *   dot  = sequential fmaf chain over t (OpenBLAS sgemm, kmeans.py:61)
+ *   norm = einsum("ij,ij->i"): sequential fl(acc + fl(v_t^2)) for n <= 3,
+ *          fl(fl(v0^2 + v1^2) + fl(v2^2 + v3^2)) for n = 4 (kmeans.py:58,64)
+ *   dist = fl(fl(fl(-2 dot) + cn) + xn), max(dist, 0), first argmin
+ *          (kmeans.py:62-67).  Defined for sub_d <= 4 only. */
+static float einsum_sq(const float *v, int n) {
+    if (n == 4) {
+        float a = v[0] * v[0], b = v[1] * v[1], c = v[2] * v[2], e = v[3] * v[3];
+        float s0 = a + b, s1 = c + e;
+        return s0 + s1;
+    }
+    float acc = v[0] * v[0];
+    for (int t = 1; t < n; ++t) {
+        float sq = v[t] * v[t];
+        acc = acc + sq;
+    }
+    return acc;
+}
+
+int orc_pq_encode(const float *X, int64_t n, int d, const float *centers, int s, int n_codes, uint8_t *out) {
+    int sub = d / s;
+    if (sub < 1 || sub > 4 || sub * s != d) return -1;
+    float *cn = (float *)malloc(sizeof(float) * (size_t)s * n_codes);
+    for (int64_t e = 0; e < (int64_t)s * n_codes; ++e) cn[e] = einsum_sq(centers + e * sub, sub);
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) {
+        for (int j = 0; j < s; ++j) {
+            const float *x = X + i * d + j * sub;
+            float xn = einsum_sq(x, sub);
+            float best = INFINITY;
+            int bi = 0;
+            for (int m = 0; m < n_codes; ++m) {
+                const float *c = centers + ((int64_t)j * n_codes + m) * sub;
+                float dot = 0.0f;
+                for (int t = 0; t < sub; ++t) dot = fmaf(x[t], c[t], dot);
+                float dist = -2.0f * dot;
+                dist = dist + cn[(int64_t)j * n_codes + m];
+                dist = dist + xn;
+                if (dist < 0.0f) dist = 0.0f;
+                if (dist < best) {
+                    best = dist;
+                    bi = m;
+                }
+            }
+            out[i * s + j] = (uint8_t)bi;
+        }
+    }
+    free(cn);
+    return 0;
+}

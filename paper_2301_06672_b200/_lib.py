@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libivfpq_b200.so")
+# IVFPQ_LIB: alternative build of the same library (kernel experiments only)
+LIB_PATH = os.environ.get("IVFPQ_LIB") or os.path.join(HERE, "libivfpq_b200.so")
 
 OK, EINVAL, ECUDA, EUNSUPPORTED = 0, 1, 2, 3
 LUT_CODES = {"f32": 0, "f16": 1, "e5m3": 2, "e4m4": 3}
@@ -49,6 +50,10 @@ SIGNATURES = {
     "ivfpq_scan_list": [_P, _I64, _I64, _I64, _P, _I32, _P],
     "ivfpq_select_clusters": [_P, _P, _I64, _I64, _P],
     "ivfpq_top_k": [_P, _P, _I64, _I64, _P, _P],
+    "ivfpq_pq_encode_device": [_P, _I64, _I64, _P, _P, _P, _I64, _I64, _P, _P],
+    "ivfpq_pq_encode": [_P, _I64, _I64, _P, _I64, _I64, _P],
+    "ivfpq_assign_device": [_P, _I64, _I64, _P, _I64, _P, _P, _P],
+    "ivfpq_assign": [_P, _I64, _I64, _P, _I64, _P, _P],
 }
 _RESTYPES = {"ivfpq_last_error": ctypes.c_char_p}
 

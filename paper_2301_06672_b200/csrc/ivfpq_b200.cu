@@ -18,6 +18,7 @@
 #include "codec.cuh"
 #include "coarse.cuh"
 #include "coarse_tc.cuh"
+#include "ingest.cuh"
 #include "scan.cuh"
 #include "topk.cuh"
 #include "ws_launch.cuh"
@@ -1208,6 +1209,103 @@ int ivfpq_top_k(const int64_t* ids, const float* dists, int64_t n, int64_t k, in
     const int64_t m = std::min(n, k);
     CK(cudaMemcpy(out_ids, doi.p, m * 8, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(out_dists, dod.p, m * 4, cudaMemcpyDeviceToHost));
+    return IVFPQ_OK;
+}
+
+}  // extern "C"
+
+// ---- ingest: pq_encode / assign_to_centroids (ingest.cuh) ---------------------
+namespace {
+template <int SUB_D>
+int launch_pq_encode(const float* x, int64_t n, int d, const float* coarse, const int64_t* assign,
+                     const float* centers, int s, int N, uint8_t* codes, cudaStream_t st) {
+    constexpr int CS = SUB_D <= 3 ? 4 : 8;
+    const size_t smem = (size_t)ENC_JG * N * CS * 4;
+    CKR(set_smem_attr((const void*)pq_encode_kernel<SUB_D>, smem));
+    const dim3 grid((unsigned)((n + ENC_THREADS - 1) / ENC_THREADS), (unsigned)((s + ENC_JG - 1) / ENC_JG));
+    pq_encode_kernel<SUB_D><<<grid, ENC_THREADS, smem, st>>>(x, n, d, coarse, assign, centers, s, N, codes);
+    KCHECK();
+    return IVFPQ_OK;
+}
+
+int check_encode_shape(int64_t n, int64_t d, int64_t s, int64_t p) {
+    if (n < 0) return set_err(IVFPQ_EINVAL, "n must be non-negative");
+    if (p < 1 || p > 8) return set_err(IVFPQ_EINVAL, "p must be in 1..8 (one byte per sub-code)");
+    if (s < 1 || d % s != 0) return set_err(IVFPQ_EINVAL, "d=%lld not divisible by s=%lld", (long long)d, (long long)s);
+    if (d / s > 4)
+        return set_err(IVFPQ_EUNSUPPORTED, "bit-exact pq_encode is implemented for sub_d <= 4 (got %lld)",
+                       (long long)(d / s));
+    if (n >= (1LL << 31) * ENC_THREADS) return set_err(IVFPQ_EUNSUPPORTED, "too many rows");
+    return IVFPQ_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int ivfpq_pq_encode_device(const float* d_x, int64_t n, int64_t d, const float* d_coarse, const int64_t* d_assign,
+                           const float* d_centers, int64_t s, int64_t p, uint8_t* d_codes, void* stream) {
+    CKR(check_encode_shape(n, d, s, p));
+    if ((d_coarse == nullptr) != (d_assign == nullptr))
+        return set_err(IVFPQ_EINVAL, "coarse and assign must be given together");
+    if (n == 0) return IVFPQ_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int N = 1 << p;
+    switch (d / s) {
+        case 1: return launch_pq_encode<1>(d_x, n, (int)d, d_coarse, d_assign, d_centers, (int)s, N, d_codes, st);
+        case 2: return launch_pq_encode<2>(d_x, n, (int)d, d_coarse, d_assign, d_centers, (int)s, N, d_codes, st);
+        case 3: return launch_pq_encode<3>(d_x, n, (int)d, d_coarse, d_assign, d_centers, (int)s, N, d_codes, st);
+        default: return launch_pq_encode<4>(d_x, n, (int)d, d_coarse, d_assign, d_centers, (int)s, N, d_codes, st);
+    }
+}
+
+int ivfpq_pq_encode(const float* x, int64_t n, int64_t d, const float* centers, int64_t s, int64_t p,
+                    uint8_t* codes) {
+    CKR(check_encode_shape(n, d, s, p));
+    if (n == 0) return IVFPQ_OK;
+    Tmp<float> dx, dc;
+    Tmp<uint8_t> dk;
+    CK(dx.alloc(n * d));
+    CK(dc.alloc((s << p) * (d / s)));
+    CK(dk.alloc(n * s));
+    CK(cudaMemcpy(dx.p, x, n * d * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dc.p, centers, (size_t)(s << p) * (d / s) * 4, cudaMemcpyHostToDevice));
+    CKR(ivfpq_pq_encode_device(dx.p, n, d, nullptr, nullptr, dc.p, s, p, dk.p, nullptr));
+    CK(cudaMemcpy(codes, dk.p, n * s, cudaMemcpyDeviceToHost));
+    return IVFPQ_OK;
+}
+
+int ivfpq_assign_device(const float* d_x, int64_t n, int64_t d, const float* d_c, int64_t nc, int64_t* d_assign,
+                        float* d_d2, void* stream) {
+    if (n < 0 || d < 1) return set_err(IVFPQ_EINVAL, "invalid data shape");
+    if (nc < 1) return set_err(IVFPQ_EINVAL, "need at least one centroid");
+    if (nc >= (1LL << 31) || n >= (1LL << 31) * AS_TM) return set_err(IVFPQ_EUNSUPPORTED, "too many rows");
+    if (n == 0) return IVFPQ_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    Tmp<float> cn;
+    CK(cn.alloc(nc));
+    row_sqnorm_kernel<<<blocks_for(nc), 256, 0, st>>>(d_c, nc, (int)d, cn.p);
+    KCHECK();
+    assign_kernel<<<(unsigned)((n + AS_TM - 1) / AS_TM), 256, 0, st>>>(d_x, n, (int)d, d_c, (int)nc, cn.p, d_assign,
+                                                                        d_d2);
+    KCHECK();
+    CK(cudaStreamSynchronize(st));  // cn is freed on return
+    return IVFPQ_OK;
+}
+
+int ivfpq_assign(const float* x, int64_t n, int64_t d, const float* c, int64_t nc, int64_t* assign, float* d2) {
+    if (n < 0 || d < 1) return set_err(IVFPQ_EINVAL, "invalid data shape");
+    if (n == 0) return IVFPQ_OK;
+    Tmp<float> dx, dc, dd;
+    Tmp<int64_t> da;
+    CK(dx.alloc(n * d));
+    CK(dc.alloc(nc * d));
+    CK(da.alloc(n));
+    CK(dd.alloc(n));
+    CK(cudaMemcpy(dx.p, x, n * d * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dc.p, c, nc * d * 4, cudaMemcpyHostToDevice));
+    CKR(ivfpq_assign_device(dx.p, n, d, dc.p, nc, da.p, dd.p, nullptr));
+    CK(cudaMemcpy(assign, da.p, n * 8, cudaMemcpyDeviceToHost));
+    if (d2) CK(cudaMemcpy(d2, dd.p, n * 4, cudaMemcpyDeviceToHost));
     return IVFPQ_OK;
 }
 

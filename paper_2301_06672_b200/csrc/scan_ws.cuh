@@ -164,6 +164,12 @@ __device__ __forceinline__ void mbar_arrive(u64* bar) {
 // Critical-path wait (builders / scanners): try_wait with a suspend-time
 // hint -- the warp parks in NANOSLEEP.SYNCS and is woken by barrier traffic
 // (measured faster than a plain spin or a timed backoff here).
+// Builders waiting for a free LUT slot: 0 = suspend-hint wait, N > 0 =
+// exponential nanosleep backoff capped at N ns (does not spin on the issue
+// slots the scanners need).
+#ifndef WS_BUILDER_BACKOFF
+#define WS_BUILDER_BACKOFF 0
+#endif
 #ifndef WS_WAIT_HINT_NS
 #define WS_WAIT_HINT_NS 1000000
 #endif
@@ -1081,7 +1087,13 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
             }
             {
                 WS_T0();
-                if (wrapped) mbar_wait(empty + slot, eph);
+                if (wrapped) {
+#if WS_BUILDER_BACKOFF > 0
+                    mbar_wait_backoff<WS_BUILDER_BACKOFF>(empty + slot, eph);
+#else
+                    mbar_wait(empty + slot, eph);
+#endif
+                }
                 WS_ACC(1);
             }
             const WsJob* PJ = pjobs + ps;

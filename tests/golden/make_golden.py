@@ -23,7 +23,8 @@ sys.path.insert(0, "/root/reference/pkg/src")
 from ivfpq8 import minifloat  # noqa: E402
 from ivfpq8.datasets import brute_force_knn, synth_gaussian_mixture  # noqa: E402
 from ivfpq8.index import build_index, save_index  # noqa: E402
-from ivfpq8.pq import train_pq  # noqa: E402
+from ivfpq8.kmeans import assign_to_centroids  # noqa: E402
+from ivfpq8.pq import PQCodebook, compute_residuals, pq_encode, train_pq  # noqa: E402
 from ivfpq8.search import SearchParams, build_lut, scan_list, search_batch, select_clusters  # noqa: E402
 
 PRECS = ["f32", "f16", "e5m3", "e4m4"]
@@ -94,8 +95,56 @@ def codec():
     print("codec", x.shape[0])
 
 
+def pq_encode_golden():
+    """pq_encode (pq.py:92-110) on inputs that stress its rounding: residual
+    sub-vectors at exact codewords (dist clipped at 0), one ulp off them, at
+    midpoints of codeword pairs, duplicated codewords (ties -> lower code),
+    plus random rows.  `exact64` counts rows where a float64 argmin would
+    disagree -- proof the fixture discriminates the fp32 recipe."""
+    rng = np.random.default_rng(77)
+    out = {}
+    for sub, p in [(1, 8), (2, 8), (3, 8), (4, 8), (4, 5), (2, 6)]:
+        s, n_codes = 12, 1 << p
+        C = (rng.standard_normal((s, n_codes, sub)) * 0.3).astype(np.float32)
+        C[:, n_codes - 1] = C[:, 3]          # duplicated codeword
+        C[:, 7] = C[:, 2] * np.float32(1.0000001)
+        rows = []
+        n = 500
+        X = (rng.standard_normal((n, s * sub)) * 0.3).astype(np.float32)
+        rows.append(X)
+        pick = rng.integers(0, n_codes, (n, s))
+        Xc = np.stack([C[j, pick[:, j]] for j in range(s)], 1).reshape(n, -1)
+        rows.append(Xc)                                                  # exact codewords
+        rows.append(np.nextafter(Xc, np.float32(np.inf)))                # one ulp off
+        pick2 = rng.integers(0, n_codes, (n, s))
+        Xm = np.stack([(C[j, pick[:, j]] + C[j, pick2[:, j]]) * np.float32(0.5) for j in range(s)], 1).reshape(n, -1)
+        rows.append(Xm.astype(np.float32))                               # midpoints
+        X = np.ascontiguousarray(np.concatenate(rows).astype(np.float32))
+        codes = pq_encode(X, PQCodebook(centers=C, p=p))
+        # float64 argmin (direct form) for the discrimination count
+        d64 = ((X.reshape(X.shape[0], s, 1, sub).astype(np.float64) - C[None].astype(np.float64)) ** 2).sum(3)
+        exact64 = int((d64.argmin(2) != codes).sum())
+        key = f"sub{sub}_p{p}"
+        out[f"{key}_x"], out[f"{key}_centers"], out[f"{key}_codes"] = X, C, codes
+        out[f"{key}_exact64"] = np.int64(exact64)
+        print("pq_encode", key, X.shape, "rows differing from a float64 argmin:", exact64)
+    # fused residual path: data - coarse[assign] (compute_residuals, pq.py:54-63)
+    data = synth_gaussian_mixture(3000, 24, 8, 0.3, seed=15)
+    coarse = data[rng.choice(3000, 16, replace=False)].copy()
+    assign, d2 = assign_to_centroids(data, coarse)
+    res = compute_residuals(data, coarse, assign)
+    C = (rng.standard_normal((8, 256, 3)) * 0.2).astype(np.float32)
+    out.update(res_data=data, res_coarse=coarse, res_assign=assign, res_d2=d2, res_centers=C,
+               res_codes=pq_encode(res, PQCodebook(centers=C, p=8)))
+    np.savez_compressed(os.path.join(HERE, "pq_encode.npz"), **out)
+
+
 def main():
+    if sys.argv[1:] == ["--only", "pq_encode"]:
+        pq_encode_golden()
+        return
     codec()
+    pq_encode_golden()
 
     # test_search.py:23-26 small_index + queries of test_search.py:202
     data = synth_gaussian_mixture(2000, 16, 8, 0.05, seed=21)
