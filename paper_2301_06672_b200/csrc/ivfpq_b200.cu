@@ -567,10 +567,6 @@ bool ws_plan(const ivfpq_index* idx, int64_t P, int64_t K, int dt, WsPlan* plan)
                                      2, (int)K, 2, (int)idx->s_pad).lut_each;
     int G = (int)std::max<size_t>(1, std::min<size_t>(WS_MAX_G, lut_budget_bytes() / lut_each));
     G = (int)std::min<int64_t>(G, std::max<int64_t>(1, P));
-    static const int env_sd = [] {
-        const char* e = getenv("IVFPQ_WS_SD");
-        return e ? atoi(e) : 0;
-    }();
     static const int env_nb = [] {
         const char* e = getenv("IVFPQ_WS_NBUF");
         return e ? atoi(e) : 0;
@@ -582,7 +578,7 @@ bool ws_plan(const ivfpq_index* idx, int64_t P, int64_t K, int dt, WsPlan* plan)
     const int G0 = G;
     for (int min_nb = 3; min_nb >= 2; --min_nb)
     for (G = G0; G >= (min_nb == 3 ? 2 : 1); --G)
-        for (int sd = env_sd ? env_sd : WS_MAX_SD; sd >= 2; --sd)
+        for (int sd = 0; sd <= 0; ++sd)  // codes go L2 -> registers: no smem stages
             for (int nb = env_nb ? env_nb : WS_MAX_NBUF; nb >= min_nb; --nb) {
                 const size_t sm = WsLayout((int)idx->d, (int)idx->s, (int)idx->sub_d, (int)idx->p, lut_bytes_of((int)dt),
                                            G, nb, (int)K, sd, (int)idx->s_pad).total;

@@ -56,7 +56,10 @@ constexpr int WS_MAX_NBUF = 6;
 constexpr int WS_NQS = 4;                    // per-query states (query top-k lists) in flight
 constexpr int WS_PD = 8;                     // prep ring depth (jobs prepared ahead)
 constexpr int WS_MAX_SD = 3;                 // code-block stages per scanner warp
-constexpr int WS_WBUF = 64;                  // per-warp candidate buffer
+#ifndef WS_WBUF_CFG
+#define WS_WBUF_CFG 64
+#endif
+constexpr int WS_WBUF = WS_WBUF_CFG;         // per-warp candidate buffer
 constexpr int WS_MAX_K = 512;
 constexpr int WS_BAR_BUILD = 1;              // named barrier id for builders
 
@@ -306,7 +309,7 @@ __device__ __forceinline__ void tmem_st(uint32_t taddr, const uint32_t (&r)[X]) 
 struct WsLayout {
     // lut rows are padded to R * jpt (jpt = ceil(s / R)) so every builder
     // thread runs the same number of rows; rq vectors likewise to R*jpt*sub_d.
-    size_t bars, sbars, qfree, tmem, jobs, pjobs, prepq, qst, lists, wbuf, prq, stage, stage_bytes, lut, total, lut_each, d_pad;
+    size_t bars, sbars, qfree, tmem, cnt, jobs, pjobs, prepq, qst, lists, wbuf, prq, stage, stage_bytes, lut, total, lut_each, d_pad;
     __host__ __device__ WsLayout(int d, int s, int sub_d, int logn, int esize, int G, int NBUF, int K, int SD, int s_pad) {
         const int N = 1 << logn, R = WS_R(N), jpt = (s + R - 1) / R;
         lut_each = (((size_t)R * jpt * N * esize) + 255) & ~(size_t)255;  // 256-aligned (PRMT addressing)
@@ -315,7 +318,8 @@ struct WsLayout {
         sbars = (2 * WS_PD + 2 * WS_MAX_NBUF) * 8;                       // stage barriers [SW][MAX_SD]
         qfree = sbars + WS_SW * WS_MAX_SD * 8;                            // query-state free barriers [NQS]
         tmem = qfree + WS_NQS * 8;                                        // u32: TMEM base address
-        jobs = tmem + 16;                                                 // WsJob[MAX_NBUF] (LUT slots)
+        cnt = tmem + 16;                                                  // int[MAX_NBUF]: next pair of each slot
+        jobs = cnt + 32;                                                  // WsJob[MAX_NBUF] (LUT slots)
         pjobs = jobs + WS_MAX_NBUF * sizeof(WsJob);                       // WsJob[PD] (prep ring, TMA-filled)
         pjobs = (pjobs + 127) & ~(size_t)127;
         prepq = pjobs + WS_PD * sizeof(WsJob);                            // int[PD]: query state of each prep entry
@@ -650,206 +654,258 @@ __device__ __forceinline__ u64 ws_acc16x2(u64 acc, uint4 wa, uint4 wb, uint32_t 
     return acc;
 }
 
-// Block table of one job for one scanner warp, held lane-parallel: lane l
-// describes the warp's block k0 + l (job block b = sw + (k0 + l) * SW), i.e.
-// pair g and vectors [vo, vo + nb) of that pair's list.  Built once per job
-// (and per 32 blocks); per block the consumer/producer only shuffle.
-struct WsTab {
-    int g, nb, n, k0;
-    long long vo;
-    __device__ __forceinline__ void load(const WsJob* J, int sw, int lane, int k0_) {
-        const int nblk = J->nblk, ng = J->ng;
-        k0 = k0_;
-        n = nblk > sw ? (nblk - sw + WS_SW - 1) / WS_SW : 0;
-        const int b = sw + (k0 + lane) * WS_SW;
-        g = 0;
-        nb = 0;
-        vo = 0;
-        if (b < nblk) {
-            while (g + 1 < ng && b >= J->pref[g + 1]) ++g;
-            const int vstart = (b - J->pref[g]) * 32;
-            nb = min(32, J->len[g] - vstart);
-            vo = J->off[g] + vstart;
-        }
+// A pair of consecutive 32-vector blocks of one job (possibly of two lists
+// of the job), as handed to a scanner warp.
+struct WsPair {
+    uint32_t base0, base1;  // smem address of each block's LUT
+    int nb0, nb1;           // vector count of each block (nb1 = 0: no second block)
+    int vo0, vo1;           // first vector of each block (a device holds < 2^31 vectors)
+    int qs;                 // query state of the job
+};
+
+// A job's list table held lane-parallel (lane g < ng describes list g), read
+// once per job: decoding a block is a ballot + 3 shuffles, no smem round trips.
+struct WsJobTab {
+    int pref;       // first block of list `lane` (INT_MAX for lanes >= ng)
+    int len;        // its vector count
+    int off;        // its first vector
+    int nblk, qs;
+    __device__ __forceinline__ void load(const WsJob* J, int lane) {
+        const int ng = J->ng;
+        nblk = J->nblk;
+        qs = J->qs;
+        pref = lane < ng ? J->pref[lane] : 0x7fffffff;
+        len = lane < ng ? J->len[lane] : 0;
+        off = lane < ng ? (int)J->off[lane] : 0;
     }
-    // block k of the warp (caller reloads the window when k - k0 >= 32)
-    __device__ __forceinline__ void get(int k, int& gk, int& nbk, long long& vok) const {
-        const int l = k - k0;
-        gk = __shfl_sync(0xffffffffu, g, l);
-        nbk = __shfl_sync(0xffffffffu, nb, l);
-        vok = __shfl_sync(0xffffffffu, vo, l);
+    __device__ __forceinline__ void block(int b, int& g, int& nb, int& vo) const {
+        const unsigned m = __ballot_sync(0xffffffffu, pref <= b);  // prefs ascend; pref[0] = 0
+        g = 31 - __clz(m);
+        const int pg = __shfl_sync(0xffffffffu, pref, g);
+        const int lg = __shfl_sync(0xffffffffu, len, g);
+        const int og = __shfl_sync(0xffffffffu, off, g);
+        const int vstart = (b - pg) * 32;
+        nb = min(32, lg - vstart);
+        vo = og + vstart;
     }
 };
 
-// Per-warp ring of SD code-block stages filled by TMA bulk copies.  The
-// producer side (lane 0) runs ahead of the consumer across job boundaries:
-// the next job's descriptor is used as soon as its LUT-ready barrier has
-// completed (non-blocking test), never more than NBUF-1 jobs ahead, so the
-// slot it reads cannot have been recycled.
-struct WsStager {
-    uint32_t stage0;      // smem address of this warp's stage 0
-    uint32_t stage_bytes;
-    u64* sbar;            // this warp's SD stage barriers
-    int SD, NBUF, sw;
-    int issued, consumed; // blocks
-    int ps, cs, cph;      // producer stage, consumer stage, consumer phase (no runtime div/mod)
-    int pjob, pk;         // producer cursor: job, warp-block index
-    int pslot, pph;       // LUT slot of pjob and its full-barrier phase
-    bool pready, pend;
-    WsTab ptab;
+// Dynamic work distribution inside a job: lane 0 takes the next pair index
+// from the slot's counter (reset by the builders when they fill the slot), so
+// scanner warps finish a job within one pair of each other.
+__device__ __forceinline__ bool ws_grab(const WsJobTab& T, int* cnt, int slot, uint32_t slot_base, uint32_t lut_each,
+                                        int lane, WsPair& p) {
+    int k = 0;
+    if (lane == 0) k = atomicAdd(cnt + slot, 1);
+    k = __shfl_sync(0xffffffffu, k, 0);
+    if (2 * k >= T.nblk) return false;
+    p.qs = T.qs;
+    int g;
+    T.block(2 * k, g, p.nb0, p.vo0);
+    p.base0 = slot_base + (uint32_t)g * lut_each;
+    if (2 * k + 1 < T.nblk) {
+        T.block(2 * k + 1, g, p.nb1, p.vo1);
+        p.base1 = slot_base + (uint32_t)g * lut_each;
+    } else {
+        p.base1 = p.base0;
+        p.nb1 = 0;
+        p.vo1 = p.vo0;
+    }
+    return true;
+}
 
-    __device__ __forceinline__ void top_up(const ScanArgs& a, const WsJob* jobs, u64* full, int cjob, int lane) {
-        while (issued - consumed < SD && !pend) {
-            if (!pready) {
-                if (pjob >= cjob + NBUF) return;
-                if (pjob != cjob && !mbar_test(full + pslot, pph)) return;
-                const WsJob* PJ = jobs + pslot;
-                if (PJ->qs < 0) {
-                    pend = true;
-                    return;
+// Chunk c (16 codes) of this lane's vector in a block: interleaved layout, so
+// a warp's 32 loads are 512 contiguous bytes.  Straight from L2 to registers.
+__device__ __forceinline__ uint4 ws_ld_chunk(const uint8_t* codes, int vo, int nb, int s_pad, int c, int lane) {
+    if (lane < nb) return ld_stream16(codes + (long long)vo * s_pad + c * nb * 16 + lane * 16);
+    return make_uint4(0u, 0u, 0u, 0u);
+}
+
+// End of this warp's part of the job in `slot`: at the query's last job, merge
+// the warp's candidates and let the last warp write the results and free the
+// query state; then release the LUT slot.
+__device__ __forceinline__ void ws_job_end(const ScanArgs& a, const WsJob* J, WsQuery* qst, u64* lists, int K,
+                                           WarpTopK& tk, u64* qfree, u64* empty_bar, int lane) {
+    if (J->last) {
+        const int qs = J->qs;
+        WsQuery* S = qst + qs;
+        u64* qlist = lists + (size_t)qs * 2 * K;
+        if (tk.n > 0) tk.flush(S, qlist, K);
+        int d = 0;
+        if (lane == 0) d = atomicAdd(&S->done, 1);
+        d = __shfl_sync(0xffffffffu, d, 0);
+        if (d == WS_SW - 1) {
+            __threadfence_block();
+            const int cur = *(volatile int*)&S->cur;
+            const u64* r = qlist + (size_t)cur * K;
+            const int q = S->q;
+            const long long nc = S->ncand;
+            for (int i = lane; i < K; i += 32) {
+                const u64 key = r[i];
+                if (a.out_keys) {
+                    a.out_keys[(size_t)q * K + i] = key;
+                } else {
+                    const bool e = key == ~0ull;
+                    a.out_ids[(size_t)q * K + i] = e ? -1LL : (long long)(uint32_t)key;
+                    a.out_dists[(size_t)q * K + i] = e ? __int_as_float(0x7f800000) : __uint_as_float((uint32_t)(key >> 32));
                 }
-                ptab.load(PJ, sw, lane, 0);
-                pk = 0;
-                pready = true;
             }
-            if (pk >= ptab.n) {
-                ++pjob;
-                if (++pslot == NBUF) {
-                    pslot = 0;
-                    pph ^= 1;
-                }
-                pready = false;
-                continue;
+            if (lane == 0) {
+                if (a.out_keys) a.out_ncand[q] = nc;
+                else a.out_short[q] = nc < K ? 1 : 0;
             }
-            if (pk - ptab.k0 >= 32) ptab.load(jobs + pslot, sw, lane, pk);
-            int g, nb;
-            long long vo;
-            ptab.get(pk, g, nb, vo);
-            if (lane == 0 && !a.debug_skip_copy) {
-                const uint32_t bytes = (uint32_t)nb * (uint32_t)a.s_pad;
-                // the stage's previous contents were consumed (values used, then
-                // __syncwarp) before this point in program order
-                mbar_expect_tx(sbar + ps, bytes);
-                bulk_g2s(stage0 + ps * stage_bytes, a.codes + (size_t)vo * a.s_pad, bytes, sbar + ps);
+            __syncwarp();
+            for (int i = lane; i < 2 * K; i += 32) qlist[i] = ~0ull;
+            __syncwarp();
+            if (lane == 0) {
+                S->tau = ~0ull;
+                S->cur = 0;
+                S->done = 0;
+                mbar_arrive(qfree + qs);  // release: state free
             }
-            ++issued;
-            ps = ps + 1 == SD ? 0 : ps + 1;
-            ++pk;
         }
     }
-};
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty_bar);
+}
 
-// Scan one job's blocks for this warp from the stage ring: R accumulated
-// sequentially in j from LUT gathers; keys under the query threshold go to
-// the warp's candidate buffer.
+// Scanner warp main loop.  Per pair: the 2 x nch chunk registers of the
+// current pair are consumed one chunk at a time and each freed register is
+// immediately refilled with the same chunk of the NEXT pair (or with chunk
+// c+4 of the current pair when nch > 4), so the L2 latency of a pair's codes
+// hides behind the scan of the previous pair.  The next pair comes from the
+// same job, else from the next job if its LUTs are already built.
 template <int DT, int LOGN>
-__device__ __forceinline__ void ws_scan_job(const ScanArgs& a, const WsJob* J, const WsJob* jobs, u64* full, int cjob,
-                                            int sw, int lane, uint32_t lut_s, uint32_t lut_each, WsQuery* S,
-                                            u64* qlist, int K, WarpTopK& tk, WsStager& sg,
-                                            unsigned long long* prof) {
+__device__ void ws_scanner(const ScanArgs& a, WsJob* jobs, int* cnt, u64* full, u64* empty, int NBUF, WsQuery* qst,
+                           u64* lists, int K, uint32_t lut_s0, uint32_t slot_bytes, uint32_t lut_each, WarpTopK& tk,
+                           u64* qfree, int lane, unsigned long long* prof) {
     constexpr int N = 1 << LOGN;
     constexpr int E = (int)sizeof(typename LutTraits<DT>::T);
-    const int nch = a.s_pad >> 4, nfull = a.s >> 4;
-#ifdef IVFPQ_WS_FINE_PROF  // fine-grained per-block timers (build with -DIVFPQ_WS_FINE_PROF)
-#define WS_P0() _p0 = prof ? clock64() : 0
-#define WS_PA(slot) \
-    do { \
-        if (prof && lane == 0) prof[slot] += (unsigned long long)(clock64() - _p0); \
-    } while (0)
-#else
-#define WS_P0() (void)_p0
-#define WS_PA(slot) (void)prof
-#endif
-    WsTab ct;
-    ct.load(J, sw, lane, 0);
-    long long _p0 = 0;
-    for (int k = 0; k < ct.n;) {
-        const bool two = k + 1 < ct.n;  // warp-uniform
-        if (k + (two ? 1 : 0) - ct.k0 >= 32) ct.load(J, sw, lane, k);
+    const int nch = a.s_pad >> 4, nfull = a.s >> 4, s_pad = a.s_pad;
+    // debug profiling (IVFPQ_WS_DEBUG bit 5): cycles in blocking LUT waits,
+    // job ends, offers/flushes, next-pair grabs
+    long long t_wait = 0, t_end = 0, t_offer = 0, t_grab = 0, _t = 0;
+#define WS_S0() _t = prof ? clock64() : 0
+#define WS_S1(acc) acc += prof ? clock64() - _t : 0
+    const uint8_t* codes = a.codes;
+    uint4 A[4], B[4];
+    uint32_t idA = 0, idB = 0;
+    int slot = 0, ph = 0;
+    WsPair cur, nxt;
+    WsJobTab ct, nt;
+    mbar_wait(full, 0);
+    if (jobs[0].qs < 0) return;
+    ct.load(jobs, lane);
+    bool have = ws_grab(ct, cnt, 0, lut_s0, lut_each, lane, cur);
+    auto load_first = [&](const WsPair& p) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (u < nch) {
+                A[u] = ws_ld_chunk(codes, p.vo0, p.nb0, s_pad, u, lane);
+                B[u] = ws_ld_chunk(codes, p.vo1, p.nb1, s_pad, u, lane);
+            }
+        idA = lane < p.nb0 ? __ldg(a.ids + p.vo0 + lane) : 0u;
+        idB = lane < p.nb1 ? __ldg(a.ids + p.vo1 + lane) : 0u;
+    };
+    if (have) load_first(cur);
+    while (true) {
+        if (!have) {
+            WS_S0();
+            ws_job_end(a, jobs + slot, qst, lists, K, tk, qfree, empty + slot, lane);
+            WS_S1(t_end);
+            if (++slot == NBUF) {
+                slot = 0;
+                ph ^= 1;
+            }
+            WS_S0();
+            mbar_wait(full + slot, ph);
+            WS_S1(t_wait);
+            if (jobs[slot].qs < 0) break;
+            ct.load(jobs + slot, lane);
+            have = ws_grab(ct, cnt, slot, lut_s0 + (uint32_t)slot * slot_bytes, lut_each, lane, cur);
+            if (have) load_first(cur);
+            continue;
+        }
+        // ---- the next pair: same job, else the next job if its LUTs are ready
+        WS_S0();
+        bool hn = ws_grab(ct, cnt, slot, lut_s0 + (uint32_t)slot * slot_bytes, lut_each, lane, nxt);
+        bool cross = false;
+        if (!hn) {
+            const int ns = slot + 1 == NBUF ? 0 : slot + 1;
+            const int nph = slot + 1 == NBUF ? ph ^ 1 : ph;
+            if (mbar_test(full + ns, (uint32_t)nph) && jobs[ns].qs >= 0) {
+                nt.load(jobs + ns, lane);
+                hn = ws_grab(nt, cnt, ns, lut_s0 + (uint32_t)ns * slot_bytes, lut_each, lane, nxt);
+                cross = true;  // (an empty next job is left to the blocking path)
+            }
+        }
+        const uint32_t nidA = hn && lane < nxt.nb0 ? __ldg(a.ids + nxt.vo0 + lane) : 0u;
+        const uint32_t nidB = hn && lane < nxt.nb1 ? __ldg(a.ids + nxt.vo1 + lane) : 0u;
+        WS_S1(t_grab);
+        // ---- scan the current pair
+        const uint32_t base0 = cur.base0, base1 = cur.base1;
+        u64 acc = pk2(0.f, 0.f);
+        for (int cg = 0; cg < nch; cg += 4) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int c = cg + u;
+                if (c < nch) {
+                    const uint32_t o = (uint32_t)(c * 16 * N * E);
+                    if (c < nfull) acc = ws_acc16x2<DT, LOGN>(acc, A[u], B[u], base0 + o, base1 + o, 16, true);
+                    else acc = ws_acc16x2<DT, LOGN>(acc, A[u], B[u], base0 + o, base1 + o, a.s - 16 * c, false);
+                    if (c + 4 < nch) {
+                        A[u] = ws_ld_chunk(codes, cur.vo0, cur.nb0, s_pad, c + 4, lane);
+                        B[u] = ws_ld_chunk(codes, cur.vo1, cur.nb1, s_pad, c + 4, lane);
+                    } else if (hn) {
+                        A[u] = ws_ld_chunk(codes, nxt.vo0, nxt.nb0, s_pad, u, lane);
+                        B[u] = ws_ld_chunk(codes, nxt.vo1, nxt.nb1, s_pad, u, lane);
+                    }
+                }
+            }
+        }
+        // ---- offers against the query's shared threshold
+        WS_S0();
         {
-            WS_P0();
-            sg.top_up(a, jobs, full, cjob, lane);
-            WS_PA(3);
-        }
-        WS_P0();
-        int g0, nb0, g1 = 0, nb1 = 0;
-        long long vo0, vo1 = 0;
-        ct.get(k, g0, nb0, vo0);
-        if (two) ct.get(k + 1, g1, nb1, vo1);
-        // ids are fetched up front; the table lookups below hide their latency
-        const uint32_t id0 =
-            lane < nb0 ? (a.debug_skip_ids ? (uint32_t)(vo0 + lane) : __ldg(a.ids + vo0 + lane)) : 0u;
-        const uint32_t id1 =
-            lane < nb1 ? (a.debug_skip_ids ? (uint32_t)(vo1 + lane) : __ldg(a.ids + vo1 + lane)) : 0u;
-        const int st0 = sg.cs;
-        const int st1 = st0 + 1 == sg.SD ? 0 : st0 + 1;
-        const uint32_t ph1 = st0 + 1 == sg.SD ? (uint32_t)(sg.cph ^ 1) : (uint32_t)sg.cph;
-        WS_PA(4);
-        {
-            WS_P0();
-            if (!a.debug_skip_copy) {
-                mbar_wait(sg.sbar + st0, sg.cph);
-                if (two) mbar_wait(sg.sbar + st1, ph1);
-            }
-            WS_PA(5);
-        }
-        WS_P0();
-        const uint32_t src0 = sg.stage0 + st0 * sg.stage_bytes + lane * 16, cs0 = (uint32_t)nb0 * 16;
-        const uint32_t base0 = lut_s + g0 * lut_each;
-        float acc0 = 0.f, acc1 = 0.f;
-        if (two) {
-            const uint32_t src1 = sg.stage0 + st1 * sg.stage_bytes + lane * 16, cs1 = (uint32_t)nb1 * 16;
-            const uint32_t base1 = lut_s + g1 * lut_each;
-            u64 acc = pk2(0.f, 0.f);
-            int c = a.debug_skip_gather ? nch : 0;  // debug bit 1
-            for (; c < nfull; ++c) {
-                const uint4 wa = lds128(src0 + c * cs0), wb = lds128(src1 + c * cs1);
-                const uint32_t o = (uint32_t)(c * 16 * N * E);
-                acc = ws_acc16x2<DT, LOGN>(acc, wa, wb, base0 + o, base1 + o, 16, true);
-            }
-            for (; c < nch; ++c) {
-                const uint4 wa = lds128(src0 + c * cs0), wb = lds128(src1 + c * cs1);
-                const uint32_t o = (uint32_t)(c * 16 * N * E);
-                acc = ws_acc16x2<DT, LOGN>(acc, wa, wb, base0 + o, base1 + o, a.s - 16 * c, false);
-            }
-            upk2(acc, acc0, acc1);
-        } else {
-            int c = a.debug_skip_gather ? nch : 0;  // debug bit 1
-            for (; c + 2 <= nfull; c += 2) {
-                const uint4 w0 = lds128(src0 + c * cs0), w1 = lds128(src0 + (c + 1) * cs0);
-                acc0 = ws_acc16<DT, LOGN>(acc0, w0, base0 + (uint32_t)(c * 16 * N * E), 16, true);
-                acc0 = ws_acc16<DT, LOGN>(acc0, w1, base0 + (uint32_t)((c + 1) * 16 * N * E), 16, true);
-            }
-            for (; c < nch; ++c) {
-                const uint4 w0 = lds128(src0 + c * cs0);
-                acc0 = ws_acc16<DT, LOGN>(acc0, w0, base0 + (uint32_t)(c * 16 * N * E), a.s - 16 * c, c < nfull);
-            }
-        }
-        __syncwarp();
-        WS_PA(6);
-        WS_P0();
-        const int used = two ? 2 : 1;
-        sg.consumed += used;
-        sg.cs += used;
-        if (sg.cs >= sg.SD) {
-            sg.cs -= sg.SD;
-            sg.cph ^= 1;
-        }
-        const u64 tau = *(volatile u64*)&S->tau;
-        const u64 key0 = ((u64)__float_as_uint(lut_finish<DT>(acc0)) << 32) | id0;
-        tk.offer(key0, lane < nb0 && key0 < tau && !a.debug_skip_gather);
-        if (tk.n > WS_WBUF - 32) tk.flush(S, qlist, K);
-        if (two) {
-            const u64 key1 = ((u64)__float_as_uint(lut_finish<DT>(acc1)) << 32) | id1;
-            tk.offer(key1, lane < nb1 && key1 < tau && !a.debug_skip_gather);
+            float r0, r1;
+            upk2(acc, r0, r1);
+            const int qs = cur.qs;
+            WsQuery* S = qst + qs;
+            u64* qlist = lists + (size_t)qs * 2 * K;
+            const u64 tau = *(volatile u64*)&S->tau;
+            const u64 k0 = ((u64)__float_as_uint(lut_finish<DT>(r0)) << 32) | idA;
+            const u64 k1 = ((u64)__float_as_uint(lut_finish<DT>(r1)) << 32) | idB;
+            tk.offer(k0, lane < cur.nb0 && k0 < tau);
+            if (tk.n > WS_WBUF - 32) tk.flush(S, qlist, K);
+            tk.offer(k1, lane < cur.nb1 && k1 < tau);
             if (tk.n > WS_WBUF - 32) tk.flush(S, qlist, K);
         }
-        WS_PA(7);
-        k += used;
+        WS_S1(t_offer);
+        if (!hn) {
+            have = false;
+            continue;
+        }
+        if (cross) {  // this warp's part of the current job is done
+            WS_S0();
+            ws_job_end(a, jobs + slot, qst, lists, K, tk, qfree, empty + slot, lane);
+            WS_S1(t_end);
+            if (++slot == NBUF) {
+                slot = 0;
+                ph ^= 1;
+            }
+            ct = nt;
+        }
+        cur = nxt;
+        idA = nidA;
+        idB = nidB;
     }
-    sg.top_up(a, jobs, full, cjob, lane);  // keep the ring busy into the next job(s)
-#undef WS_P0
-#undef WS_PA
+    if (prof && lane == 0) {
+        atomicAdd(prof + 3, (unsigned long long)t_wait);
+        atomicAdd(prof + 4, (unsigned long long)t_end);
+        atomicAdd(prof + 5, (unsigned long long)t_offer);
+        atomicAdd(prof + 6, (unsigned long long)t_grab);
+    }
+#undef WS_S0
+#undef WS_S1
 }
 
 // debug profiling: accumulate clock64 deltas per warp (lane 0) into w.prof
@@ -1036,7 +1092,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
             q = __shfl_sync(0xffffffffu, q, 0);
             const int ps0 = job % WS_PD;
             if (q >= a.nq) {
-                if (job >= WS_PD) mbar_wait(pempty + ps0, ((job / WS_PD) - 1) & 1);
+                if (job >= WS_PD) mbar_wait_backoff<256>(pempty + ps0, ((job / WS_PD) - 1) & 1);
                 if (lane == 0) {
                     pqs[ps0] = -1;
                     mbar_arrive(pfull + ps0);
@@ -1057,7 +1113,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
                 const int ps = job % WS_PD;
                 {
                     WS_T0();
-                    if (job >= WS_PD) mbar_wait(pempty + ps, ((job / WS_PD) - 1) & 1);
+                    if (job >= WS_PD) mbar_wait_backoff<256>(pempty + ps, ((job / WS_PD) - 1) & 1);
                     WS_ACC(0);
                 }
                 if (lane == 0) {
@@ -1103,7 +1159,10 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
                 int* dst = reinterpret_cast<int*>(jobs + slot);
                 for (int i = t; i < (int)(sizeof(WsJob) / 4); i += 32) dst[i] = src[i];
                 __syncwarp();
-                if (t == 0) jobs[slot].qs = pq_s;
+                if (t == 0) {
+                    jobs[slot].qs = pq_s;
+                    reinterpret_cast<int*>(smem + L.cnt)[slot] = 0;  // scanners' pair counter
+                }
             }
             if (pq_s < 0) {
                 __syncwarp();
@@ -1135,96 +1194,13 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
         const int sw = warp - WS_BW;
         u64* wb = reinterpret_cast<u64*>(smem + L.wbuf) + (size_t)sw * 2 * WS_WBUF;
         WarpTopK tk{wb, wb + WS_WBUF, 0};
-#ifdef IVFPQ_WS_FINE_PROF
-        unsigned long long wprof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-#else
-        unsigned long long* wprof = nullptr;
-#endif
-        WsStager sg;
-        sg.stage0 = smem_addr(smem + L.stage) + (uint32_t)(sw * SD * L.stage_bytes);
-        sg.stage_bytes = (uint32_t)L.stage_bytes;
-        sg.sbar = reinterpret_cast<u64*>(smem + L.sbars) + sw * WS_MAX_SD;
-        sg.SD = SD;
-        sg.NBUF = NBUF;
-        sg.sw = sw;
-        sg.issued = sg.consumed = 0;
-        sg.ps = sg.cs = sg.cph = 0;
-        sg.pslot = sg.pph = 0;
-        sg.pjob = 0;
-        sg.pk = 0;
-        sg.pready = false;
-        sg.pend = false;
-        int slot = 0, fph = 0;
-        for (int job = 0;; ++job) {
-            {
-                WS_T0();
-                mbar_wait(full + slot, fph);
-                WS_ACC(0);
-            }
-            const WsJob* J = jobs + slot;
-            const int qs = J->qs;
-            if (qs < 0) {
-#ifdef IVFPQ_WS_FINE_PROF
-                if (w.prof && lane == 0)
-                    for (int i = 3; i < 8; ++i) atomicAdd(w.prof + ((size_t)blockIdx.x * 32 + warp) * 8 + i, wprof[i]);
-#endif
-                break;
-            }
-            WsQuery* S = qst + qs;
-            u64* qlist = lists + (size_t)qs * 2 * K;
-            const uint8_t* lutb = lut_all + (size_t)slot * G * lut_each;  // rows padded; scan reads j < s
-            {
-                WS_T0();
-                if (!(w.debug & 4))
-                    ws_scan_job<DT, LOGN>(a, J, jobs, full, job, sw, lane, smem_addr(lutb), (uint32_t)lut_each, S, qlist,
-                                          K, tk, sg, w.prof ? wprof : nullptr);
-                WS_ACC(1);
-            }
+        {
             WS_T0();
-            if (J->last) {
-                if (tk.n > 0) tk.flush(S, qlist, K);
-                int d = 0;
-                if (lane == 0) d = atomicAdd(&S->done, 1);
-                d = __shfl_sync(0xffffffffu, d, 0);
-                if (d == WS_SW - 1) {
-                    // last warp for this query: results + reset of the query state
-                    __threadfence_block();
-                    const int cur = *(volatile int*)&S->cur;
-                    const u64* r = qlist + (size_t)cur * K;
-                    const int q = S->q;
-                    const long long nc = S->ncand;
-                    for (int i = lane; i < K; i += 32) {
-                        const u64 key = r[i];
-                        if (a.out_keys) {
-                            a.out_keys[(size_t)q * K + i] = key;
-                        } else {
-                            const bool e = key == ~0ull;
-                            a.out_ids[(size_t)q * K + i] = e ? -1LL : (long long)(uint32_t)key;
-                            a.out_dists[(size_t)q * K + i] = e ? __int_as_float(0x7f800000) : __uint_as_float((uint32_t)(key >> 32));
-                        }
-                    }
-                    if (lane == 0) {
-                        if (a.out_keys) a.out_ncand[q] = nc;
-                        else a.out_short[q] = nc < K ? 1 : 0;
-                    }
-                    __syncwarp();
-                    for (int i = lane; i < 2 * K; i += 32) qlist[i] = ~0ull;
-                    __syncwarp();
-                    if (lane == 0) {
-                        S->tau = ~0ull;
-                        S->cur = 0;
-                        S->done = 0;
-                        mbar_arrive(reinterpret_cast<u64*>(smem + L.qfree) + qs);  // release: state free
-                    }
-                }
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(empty + slot);
-            WS_ACC(2);
-            if (++slot == NBUF) {
-                slot = 0;
-                fph ^= 1;
-            }
+            ws_scanner<DT, LOGN>(a, jobs, reinterpret_cast<int*>(smem + L.cnt), full, empty, NBUF, qst, lists, K,
+                                 smem_addr(lut_all), (uint32_t)(G * lut_each), (uint32_t)lut_each, tk,
+                                 reinterpret_cast<u64*>(smem + L.qfree), lane,
+                                 w.prof ? w.prof + ((size_t)blockIdx.x * 32 + warp) * 8 : nullptr);
+            WS_ACC(1);
         }
     }
 }

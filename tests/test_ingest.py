@@ -73,7 +73,8 @@ def test_fused_residual_encode_and_assign(pkg, enc):
     a = a.cpu().numpy()
     # decision-level parity (einsum's norm order at d=24 is not modelled)
     assert (a != enc["res_assign"]).mean() < 1e-3
-    np.testing.assert_allclose(d2.cpu().numpy(), enc["res_d2"], rtol=1e-5, atol=1e-6)
+    # expanded-form distances cancel near 0: absolute tolerance
+    np.testing.assert_allclose(d2.cpu().numpy(), enc["res_d2"], rtol=1e-5, atol=1e-5)
     codes = pkg.ingest.pq_encode_device(x, torch.from_numpy(enc["res_centers"]).cuda(), 8, coarse,
                                         torch.from_numpy(enc["res_assign"]).cuda())
     assert np.array_equal(codes.cpu().numpy(), enc["res_codes"])
