@@ -122,26 +122,11 @@ def build_index_gpu(base: np.ndarray, nlist: int, s: int, p: int, seed: int = 0,
     return idx
 
 
-def ground_truth_gpu(base: np.ndarray, queries: np.ndarray, k: int, chunk: int = 1024, margin: int = 32):
-    """Exact k-NN (ties -> lower id): fp32 GEMM shortlist of k+margin, exact
-    fp64 re-rank of the shortlist."""
-    import torch
-    x = torch.from_numpy(base).cuda()
-    xn = (x * x).sum(1)
-    out = np.empty((queries.shape[0], k), dtype=np.int64)
-    for lo in range(0, queries.shape[0], chunk):
-        q = torch.from_numpy(queries[lo:lo + chunk]).cuda()
-        d = xn[None, :] - 2.0 * (q @ x.T)
-        cand = d.topk(k + margin, dim=1, largest=False).indices
-        exact = ((x[cand].double() - q[:, None, :].double()) ** 2).sum(2)
-        # lexicographic (distance, id): sort by id, then stable sort by distance
-        ids_sorted, perm = cand.sort(1)
-        ex = exact.gather(1, perm)
-        order = torch.sort(ex, dim=1, stable=True).indices[:, :k]
-        out[lo:lo + chunk] = ids_sorted.gather(1, order).cpu().numpy()
-    del x
-    torch.cuda.empty_cache()
-    return out
+def ground_truth_gpu(base: np.ndarray, queries: np.ndarray, k: int) -> np.ndarray:
+    """Exact k-NN ids (ties -> lower id) with the product's K7 kernel
+    (`brute_force_knn`, bit-identical to the reference's datasets.py:179-201)."""
+    from paper_2301_06672_b200.datasets import brute_force_knn
+    return brute_force_knn(base, queries, k).ids
 
 
 def recall_at(ids: np.ndarray, gt: np.ndarray) -> float:

@@ -132,6 +132,17 @@ int ivfpq_assign_device(const float *d_x, int64_t n, int64_t d, const float *d_c
                         float *d_d2, void *stream);
 int ivfpq_assign(const float *x, int64_t n, int64_t d, const float *c, int64_t nc, int64_t *assign, float *d2);
 
+/* --- K7: exact k-NN ground truth --------------------- */
+/* brute_force_knn (datasets.py:179-201): per query the k smallest
+ * squared_l2_to_all distances (datasets.py:166-176: sequential fp32 sum of
+ * fl(diff^2)), ties -> lower id; ids AND distances bit-exact with the
+ * reference.  Reuses the K1 select path over the base rows.  A handle from
+ * ivfpq_knn_create is searched with ivfpq_select_device (keys = d2 bits << 32
+ * | row id) and freed with ivfpq_index_destroy. */
+int ivfpq_knn_create(int device, const float *base, int64_t n, int64_t d, ivfpq_index **out);
+int ivfpq_brute_force_knn(const float *base, int64_t n, int64_t d, const float *queries, int64_t nq, int64_t k,
+                          int64_t *out_ids, float *out_dists);
+
 #ifdef __cplusplus
 }
 #endif

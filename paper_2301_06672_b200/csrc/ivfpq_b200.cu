@@ -1306,3 +1306,101 @@ int ivfpq_assign(const float* x, int64_t n, int64_t d, const float* c, int64_t n
 }
 
 }  // extern "C"
+
+// ---- K7: exact k-NN (brute_force_knn, datasets.py:179-201) ---------------------
+// The reference's ground truth is K1's arithmetic over the base rows instead of
+// the centroids: d2 = sequential fl(acc + fl(diff^2)) (squared_l2_to_all,
+// datasets.py:166-176), stable argsort -> (d2, id) keys.  A k-NN handle is an
+// index whose "centroids" are the base rows (no lists), searched with the
+// same select path (tensor-core nomination + exact re-rank + guard).
+extern "C" {
+
+int ivfpq_knn_create(int device, const float* base, int64_t n, int64_t d, ivfpq_index** out) {
+    if (!out) return set_err(IVFPQ_EINVAL, "null output handle");
+    *out = nullptr;
+    if (n < 1 || d < 1) return set_err(IVFPQ_EINVAL, "invalid base shape n=%lld d=%lld", (long long)n, (long long)d);
+    if (n >= (1LL << 31) - 1) return set_err(IVFPQ_EUNSUPPORTED, "base too large for one k-NN handle");
+    DeviceGuard guard(device);
+    CK(cudaSetDevice(device));
+    ivfpq_index* idx = new ivfpq_index();
+    idx->device = device;
+    idx->nlist = idx->nlist_local = n;
+    idx->d = d;
+    idx->s = 1;
+    idx->p = 1;
+    idx->sub_d = d;
+    auto fail = [&](int rc) {
+        ivfpq_index_destroy(idx);
+        return rc;
+    };
+#define CKI(call)                                                                              \
+    do {                                                                                       \
+        cudaError_t e_ = (call);                                                               \
+        if (e_ != cudaSuccess)                                                                 \
+            return fail(set_err(IVFPQ_ECUDA, "%s failed: %s", #call, cudaGetErrorString(e_))); \
+    } while (0)
+    CKI(cudaStreamCreateWithFlags(&idx->stream, cudaStreamNonBlocking));
+    CKI(cudaDeviceGetAttribute(&idx->num_sms, cudaDevAttrMultiProcessorCount, device));
+    CKI(cudaMalloc((void**)&idx->coarse, (size_t)n * d * 4));
+    CKI(cudaMemcpy(idx->coarse, base, (size_t)n * d * 4, cudaMemcpyHostToDevice));
+    std::vector<int32_t> ident(n);
+    for (int64_t i = 0; i < n; ++i) ident[i] = (int32_t)i;
+    CKI(cudaMalloc((void**)&idx->l2g, (size_t)n * 4));
+    CKI(cudaMemcpy(idx->l2g, ident.data(), (size_t)n * 4, cudaMemcpyHostToDevice));
+    idx->bytes = n * d * 4 + n * 4;
+    if (d <= TC_MAXD) {
+        const int64_t ntiles = (n + TC_N - 1) / TC_N, nkc = coarse_tc_nkc((int)d);
+        const size_t ib = (size_t)ntiles * nkc * TC_N * 128;
+        CKI(cudaMalloc((void**)&idx->tc_img, ib));
+        idx->bytes += (int64_t)ib;
+        coarse_tc_prep_kernel<<<(unsigned)ntiles, 256, 0, idx->stream>>>(idx->coarse, (int)n, (int)d, (int)nkc,
+                                                                         idx->tc_img);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        CKI(cudaGetLastError());
+        idx->tc_cmax = coarse_tc_cmax(base, n, d);
+    }
+    CKI(cudaStreamSynchronize(idx->stream));
+#undef CKI
+    *out = idx;
+    return IVFPQ_OK;
+}
+
+int ivfpq_brute_force_knn(const float* base, int64_t n, int64_t d, const float* queries, int64_t nq, int64_t k,
+                          int64_t* out_ids, float* out_dists) {
+    if (k < 1) return set_err(IVFPQ_EINVAL, "k must be at least 1");
+    if (k > n) return set_err(IVFPQ_EINVAL, "k=%lld exceeds base size %lld", (long long)k, (long long)n);
+    if (k > MAX_K) return set_err(IVFPQ_EUNSUPPORTED, "k exceeds the device limit %d", MAX_K);
+    ivfpq_index* h = nullptr;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    CKR(ivfpq_knn_create(dev, base, n, d, &h));
+    struct Closer {
+        ivfpq_index* h;
+        ~Closer() { ivfpq_index_destroy(h); }
+    } closer{h};
+    if (nq == 0) return IVFPQ_OK;
+    cudaStream_t st = h->stream;
+    const int64_t chunk = std::min<int64_t>(nq, 16384);
+    CKR(h->q.ensure((size_t)chunk * d * 4));
+    CKR(h->pkeys.ensure((size_t)chunk * k * 8));
+    CKR(h->oids.ensure((size_t)chunk * k * 8));
+    CKR(h->odist.ensure((size_t)chunk * k * 4));
+    CKR(h->ncand.ensure((size_t)chunk * 8));
+    CKR(h->oshort.ensure((size_t)chunk * 4));
+    for (int64_t q0 = 0; q0 < nq; q0 += chunk) {
+        const int64_t m = std::min(chunk, nq - q0);
+        CK(cudaMemcpyAsync(h->q.p, queries + q0 * d, (size_t)m * d * 4, cudaMemcpyHostToDevice, st));
+        CKR(run_select(h, h->q.as<float>(), m, k, h->pkeys.as<uint64_t>(), st));
+        CK(cudaMemsetAsync(h->ncand.p, 0x7f, (size_t)m * 8, st));  // never short: k <= n
+        finalize_kernel<<<blocks_for(m * k), 256, 0, st>>>(h->pkeys.as<uint64_t>(), h->ncand.as<int64_t>(), (int)m,
+                                                          (int)k, h->oids.as<int64_t>(), h->odist.as<float>(),
+                                                          h->oshort.as<int32_t>());
+        KCHECK();
+        CK(cudaMemcpyAsync(out_ids + q0 * k, h->oids.p, (size_t)m * k * 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(out_dists + q0 * k, h->odist.p, (size_t)m * k * 4, cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaStreamSynchronize(st));
+    return IVFPQ_OK;
+}
+
+}  // extern "C"
