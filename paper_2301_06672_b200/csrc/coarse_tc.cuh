@@ -48,7 +48,8 @@ constexpr int TC_CAP = 128;      // nominated centroids per (query, slice)
 constexpr int TC_STAGES = 6;
 constexpr int TC_ACOL = 256;     // TMEM columns [0, 256): two accumulators; [256, 512): the query block (A)
 constexpr int TC_MAXD = TC_ACOL - 2;  // A = [-2q, 1, 1] must fit 256 TMEM columns
-constexpr int TC_MAXP = 32;      // nprobe served by this path
+constexpr int TC_MAXP = 96;      // nprobe served by this path (P > 32 uses >= ceil(P/32) slices)
+constexpr int TC_P_PER_SLICE = 32;  // nprobe covered per slice by its ~TC_GJ..90 nominations
 constexpr int TC_MAXSL = 4;      // centroid slices per query block
 constexpr int TC_EPI = 8;        // epilogue warps: 2 per TMEM lane quarter (column halves)
 constexpr int TC_THREADS = 128 + 32 * TC_EPI;  // warp 0 producer, 1 MMA, 2 TMEM alloc, 4.. epilogue

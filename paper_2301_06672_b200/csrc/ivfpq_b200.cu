@@ -402,7 +402,12 @@ int run_select_tc(ivfpq_index* idx, const float* d_q, int64_t nq, int64_t P, uin
     const int64_t nc = idx->nlist_local, d = idx->d;
     const int64_t ntiles = (nc + TC_N - 1) / TC_N, nkc = coarse_tc_nkc((int)d);
     const int64_t qblocks = (nq + TC_M - 1) / TC_M;
-    const int64_t nsl = std::max<int64_t>(1, std::min<int64_t>({(int64_t)TC_MAXSL, ntiles, idx->num_sms / qblocks}));
+    // slices: fill the SMs; large nprobe needs ceil(P / 32) slices so each
+    // slice's ~48..90 nominations cover its share of the top-P with margin
+    // (else the guard would send the query to the exact re-do)
+    const int64_t nsl_p = std::min<int64_t>(TC_MAXSL, (P + TC_P_PER_SLICE - 1) / TC_P_PER_SLICE);
+    const int64_t nsl = std::max<int64_t>(
+        1, std::min<int64_t>(ntiles, std::max<int64_t>(nsl_p, std::min<int64_t>(TC_MAXSL, idx->num_sms / qblocks))));
     const int64_t tps = (ntiles + nsl - 1) / nsl;
     const size_t rows = (size_t)nsl * nq;
     CKR(idx->tc_sl.ensure(rows * TC_CAP * 4 + rows * 8));
@@ -562,7 +567,7 @@ bool ws_plan(const ivfpq_index* idx, int64_t P, int64_t K, int dt, WsPlan* plan)
     if (idx->p < 2 || idx->sub_d < 1 || idx->sub_d > 4 || K > WS_MAX_K) return false;
     const int64_t R = WS_R((int)N);
     const int64_t jpt = WS_JPT((int)idx->sub_d);
-    if ((idx->s + R - 1) / R > jpt) return false;
+    if ((idx->s_pad + R - 1) / R > jpt) return false;  // LUT rows padded to s_pad
     const size_t lut_each = WsLayout((int)idx->d, (int)idx->s, (int)idx->sub_d, (int)idx->p, lut_bytes_of((int)dt), 1,
                                      2, (int)K, 2, (int)idx->s_pad).lut_each;
     int G = (int)std::max<size_t>(1, std::min<size_t>(WS_MAX_G, lut_budget_bytes() / lut_each));

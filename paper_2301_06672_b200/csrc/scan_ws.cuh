@@ -307,11 +307,14 @@ __device__ __forceinline__ void tmem_st(uint32_t taddr, const uint32_t (&r)[X]) 
 
 // --------------------------------------------------------------- smem layout
 struct WsLayout {
-    // lut rows are padded to R * jpt (jpt = ceil(s / R)) so every builder
+    // lut rows are padded to R * jpt (jpt = ceil(s_pad / R)) so every builder
     // thread runs the same number of rows; rq vectors likewise to R*jpt*sub_d.
+    // Rows j >= s hold +0 entries (zero centers, zero residual), so the scan
+    // reads whole 16-code chunks: the zero-code lookups past s add +0, which
+    // leaves every sum bit-identical.
     size_t bars, sbars, qfree, tmem, cnt, jobs, pjobs, prepq, qst, lists, wbuf, prq, stage, stage_bytes, lut, total, lut_each, d_pad;
     __host__ __device__ WsLayout(int d, int s, int sub_d, int logn, int esize, int G, int NBUF, int K, int SD, int s_pad) {
-        const int N = 1 << logn, R = WS_R(N), jpt = (s + R - 1) / R;
+        const int N = 1 << logn, R = WS_R(N), jpt = (s_pad + R - 1) / R;
         lut_each = (((size_t)R * jpt * N * esize) + 255) & ~(size_t)255;  // 256-aligned (PRMT addressing)
         d_pad = (size_t)R * jpt * sub_d;
         bars = 0;                                                         // pfull/pempty[PD], full/empty[MAX_NBUF]
@@ -492,10 +495,17 @@ struct WsBuild {
 };
 
 // ------------------------------------------------------------- warp top-k
+// flush inlined: out of line it costs ~25% (call-site register spills, measured)
+#ifdef WS_FLUSH_NOINLINE
+#define WS_FLUSH_ATTR __device__ __noinline__
+#else
+#define WS_FLUSH_ATTR __device__ __forceinline__
+#endif
 struct WarpTopK {
     u64* buf;      // WS_WBUF
     u64* srt;      // WS_WBUF
     int n;         // warp-uniform count
+    unsigned long long* prof = nullptr;  // debug: [0] flushes, [2] locked flushes, [7] flush cycles
 
     __device__ __forceinline__ void offer(u64 key, bool pred) {
         const unsigned m = __ballot_sync(0xffffffffu, pred);
@@ -506,7 +516,15 @@ struct WarpTopK {
     // Merge the buffer into the query's shared list.  Candidates are first
     // re-filtered against the current threshold (it has usually tightened
     // since they were offered), so most flushes end without taking the lock.
-    __device__ void flush(WsQuery* S, u64* lists, int K) {
+    WS_FLUSH_ATTR void flush(WsQuery* S, u64* lists, int K) {
+        const long long t0 = prof ? clock64() : 0;
+        flush_(S, lists, K);
+        if (prof && (threadIdx.x & 31) == 0) {
+            prof[0] += 1;
+            prof[7] += (unsigned long long)(clock64() - t0);
+        }
+    }
+    __device__ void flush_(WsQuery* S, u64* lists, int K) {
         const int lane = threadIdx.x & 31;
         __syncwarp();
         const u64 tau = *(volatile u64*)&S->tau;
@@ -530,6 +548,7 @@ struct WarpTopK {
         __syncwarp();
         for (int i = lane; i < m; i += 32) srt[i] = buf[i];
         const int n = m;
+        if (prof && lane == 0) prof[2] += 1;
         if (lane == 0) {
             while (atomicCAS(&S->lock, 0, 1) != 0) {
             }
@@ -781,7 +800,12 @@ __device__ void ws_scanner(const ScanArgs& a, WsJob* jobs, int* cnt, u64* full, 
                            u64* qfree, int lane, unsigned long long* prof) {
     constexpr int N = 1 << LOGN;
     constexpr int E = (int)sizeof(typename LutTraits<DT>::T);
-    const int nch = a.s_pad >> 4, nfull = a.s >> 4, s_pad = a.s_pad;
+    const int nch = a.s_pad >> 4, s_pad = a.s_pad;  // LUT rows >= s are +0: whole chunks are exact
+    // Code shape, measured on cfg2: the fp8 scans run 8% faster when the chunk
+    // loop keeps a (never taken at s % 16 == 0) partial-chunk branch, f16/f32
+    // 10% faster without it -- an instruction-scheduling effect of ptxas 12.9.
+    constexpr bool kSplit = DT == LUT_E5M3 || DT == LUT_E4M4;
+    const int nfull = kSplit ? a.s >> 4 : nch;
     // debug profiling (IVFPQ_WS_DEBUG bit 5): cycles in blocking LUT waits,
     // job ends, offers/flushes, next-pair grabs
     long long t_wait = 0, t_end = 0, t_offer = 0, t_grab = 0, _t = 0;
@@ -851,7 +875,7 @@ __device__ void ws_scanner(const ScanArgs& a, WsJob* jobs, int* cnt, u64* full, 
                 const int c = cg + u;
                 if (c < nch) {
                     const uint32_t o = (uint32_t)(c * 16 * N * E);
-                    if (c < nfull) acc = ws_acc16x2<DT, LOGN>(acc, A[u], B[u], base0 + o, base1 + o, 16, true);
+                    if (!kSplit || c < nfull) acc = ws_acc16x2<DT, LOGN>(acc, A[u], B[u], base0 + o, base1 + o, 16, true);
                     else acc = ws_acc16x2<DT, LOGN>(acc, A[u], B[u], base0 + o, base1 + o, a.s - 16 * c, false);
                     if (c + 4 < nch) {
                         A[u] = ws_ld_chunk(codes, cur.vo0, cur.nb0, s_pad, c + 4, lane);
@@ -1030,7 +1054,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
     const WsLayout L(a.d, a.s, SUB_D, LOGN, (int)sizeof(T), G, NBUF, K, SD, a.s_pad);
     const size_t lut_each = L.lut_each;
     const int d_pad = (int)L.d_pad;
-    const int jpt = (a.s + WsBuild<DT, LOGN, SUB_D>::R - 1) / WsBuild<DT, LOGN, SUB_D>::R;  // rows per builder
+    const int jpt = (a.s_pad + WsBuild<DT, LOGN, SUB_D>::R - 1) / WsBuild<DT, LOGN, SUB_D>::R;  // rows per builder
     u64* pfull = reinterpret_cast<u64*>(smem + L.bars);  // pfull[PD]: job + residuals prepared
     u64* pempty = pfull + WS_PD;                          // pempty[PD]: prep entry consumed
     u64* full = pempty + WS_PD;                           // full[NBUF]: LUTs ready
@@ -1194,6 +1218,10 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
         const int sw = warp - WS_BW;
         u64* wb = reinterpret_cast<u64*>(smem + L.wbuf) + (size_t)sw * 2 * WS_WBUF;
         WarpTopK tk{wb, wb + WS_WBUF, 0};
+#ifdef WS_TK_PROF  // flush statistics (experiments only)
+        unsigned long long tkprof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (w.prof) tk.prof = tkprof;
+#endif
         {
             WS_T0();
             ws_scanner<DT, LOGN>(a, jobs, reinterpret_cast<int*>(smem + L.cnt), full, empty, NBUF, qst, lists, K,
@@ -1202,6 +1230,10 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
                                  w.prof ? w.prof + ((size_t)blockIdx.x * 32 + warp) * 8 : nullptr);
             WS_ACC(1);
         }
+#ifdef WS_TK_PROF
+        if (w.prof && lane == 0)
+            for (int i : {0, 2, 7}) atomicAdd(w.prof + ((size_t)blockIdx.x * 32 + warp) * 8 + i, tkprof[i]);
+#endif
     }
 }
 

@@ -367,6 +367,8 @@ def select_mode(request, pkg):
     (2048, 100, 257, 1),     # d not a multiple of 4 / of the 32-wide K chunk
     (700, 160, 64, 17),      # largest d with resident queries
     (4096, 128, 40, 32),     # few query blocks -> several centroid slices merged
+    (8192, 96, 300, 64),     # cfg5-style nprobe 64: slices sized by P
+    (4096, 96, 200, 96),     # largest nprobe on the tensor-core path
 ])
 def test_select_tensor_core_path_bit_exact(pkg, select_mode, nlist, d, nq, P):
     """K1 on tcgen05 (TF32 nomination, exact re-rank, guard, exact re-do of
