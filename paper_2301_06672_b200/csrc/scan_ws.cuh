@@ -712,7 +712,11 @@ struct WsJobTab {
 // Dynamic work distribution inside a job: lane 0 takes the next pair index
 // from the slot's counter (reset by the builders when they fill the slot), so
 // scanner warps finish a job within one pair of each other.
-__device__ __forceinline__ bool ws_pair(const WsJobTab& T, int k, uint32_t slot_base, uint32_t lut_each, WsPair& p) {
+__device__ __forceinline__ bool ws_grab(const WsJobTab& T, int* cnt, int slot, uint32_t slot_base, uint32_t lut_each,
+                                        int lane, WsPair& p) {
+    int k = 0;
+    if (lane == 0) k = atomicAdd(cnt + slot, 1);
+    k = __shfl_sync(0xffffffffu, k, 0);
     if (2 * k >= T.nblk) return false;
     p.qs = T.qs;
     int g;
@@ -816,16 +820,7 @@ __device__ void ws_scanner(const ScanArgs& a, WsJob* jobs, int* cnt, u64* full, 
     mbar_wait(full, 0);
     if (jobs[0].qs < 0) return;
     ct.load(jobs, lane);
-    // Pair indices are taken from the slot counter one pair AHEAD: the atomic
-    // issued now is consumed at the next pair, so its latency is hidden.
-    int kpre = 0;  // lane 0: pair index prefetched from the current slot
-    auto issue = [&](int sl) {
-        if (lane == 0) kpre = atomicAdd(cnt + sl, 1);
-    };
-    auto take = [&]() { return __shfl_sync(0xffffffffu, kpre, 0); };
-    issue(0);
-    bool have = ws_pair(ct, take(), lut_s0, lut_each, cur);
-    if (have) issue(0);
+    bool have = ws_grab(ct, cnt, 0, lut_s0, lut_each, lane, cur);
     auto load_first = [&](const WsPair& p) {
 #pragma unroll
         for (int u = 0; u < 4; ++u)
@@ -851,25 +846,20 @@ __device__ void ws_scanner(const ScanArgs& a, WsJob* jobs, int* cnt, u64* full, 
             WS_S1(t_wait);
             if (jobs[slot].qs < 0) break;
             ct.load(jobs + slot, lane);
-            issue(slot);
-            have = ws_pair(ct, take(), lut_s0 + (uint32_t)slot * slot_bytes, lut_each, cur);
-            if (have) issue(slot);
+            have = ws_grab(ct, cnt, slot, lut_s0 + (uint32_t)slot * slot_bytes, lut_each, lane, cur);
             if (have) load_first(cur);
             continue;
         }
         // ---- the next pair: same job, else the next job if its LUTs are ready
         WS_S0();
-        bool hn = ws_pair(ct, take(), lut_s0 + (uint32_t)slot * slot_bytes, lut_each, nxt);
-        if (hn) issue(slot);
+        bool hn = ws_grab(ct, cnt, slot, lut_s0 + (uint32_t)slot * slot_bytes, lut_each, lane, nxt);
         bool cross = false;
         if (!hn) {
             const int ns = slot + 1 == NBUF ? 0 : slot + 1;
             const int nph = slot + 1 == NBUF ? ph ^ 1 : ph;
             if (mbar_test(full + ns, (uint32_t)nph) && jobs[ns].qs >= 0) {
                 nt.load(jobs + ns, lane);
-                issue(ns);
-                hn = ws_pair(nt, take(), lut_s0 + (uint32_t)ns * slot_bytes, lut_each, nxt);
-                if (hn) issue(ns);
+                hn = ws_grab(nt, cnt, ns, lut_s0 + (uint32_t)ns * slot_bytes, lut_each, lane, nxt);
                 cross = true;  // (an empty next job is left to the blocking path)
             }
         }
