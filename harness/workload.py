@@ -3,9 +3,10 @@ ground truth.  Harness code, not the product: it uses torch ops as plumbing to
 produce the inputs of the search path quickly at BASELINE.json sizes.
 
 Index training is OUT OF SCOPE for the hot path:
-coarse k-means and per-subspace PQ k-means here are plain Lloyd iterations on
-a subsample; assignment/encoding take the nearest centroid.  The search
-kernels consume the resulting arrays exactly like a reference-built index.
+the index comes from the package's GPU builder (Lloyd iterations on a
+subsample; assignment and bit-exact PQ encoding by the product kernels).  The
+search kernels consume the resulting arrays exactly like a reference-built
+index.
 """
 
 from __future__ import annotations
@@ -41,85 +42,13 @@ def make_data(cfg):
     return X[:cfg["n"]], X[cfg["n"]:]
 
 
-def _nearest(x, c, chunk=65536):
-    """argmin_j ||x_i - c_j||^2 (expanded form, fp32 tensor cores off)."""
-    import torch
-    cn = (c * c).sum(1)
-    out = torch.empty(x.shape[0], dtype=torch.int64, device=x.device)
-    for lo in range(0, x.shape[0], chunk):
-        xb = x[lo:lo + chunk]
-        d = cn[None, :] - 2.0 * (xb @ c.T)
-        out[lo:lo + chunk] = d.argmin(1)
-    return out
-
-
-def _segment_means(x, a, k, old):
-    """Deterministic per-cluster means (sort + float64 prefix sums; no atomics)."""
-    import torch
-    order = torch.sort(a, stable=True).indices
-    cs = torch.zeros((x.shape[0] + 1, x.shape[1]), dtype=torch.float64, device=x.device)
-    cs[1:] = torch.cumsum(x[order].double(), 0)
-    cnt = torch.bincount(a, minlength=k)
-    hi = torch.cumsum(cnt, 0)
-    lo = hi - cnt
-    sums = cs[hi] - cs[lo]
-    return torch.where(cnt[:, None] > 0, (sums / cnt.clamp(min=1)[:, None]).float(), old)
-
-
-def _kmeans(x, k, iters, seed):
-    import torch
-    g = torch.Generator(device=x.device).manual_seed(seed)
-    c = x[torch.randperm(x.shape[0], generator=g, device=x.device)[:k]].clone()
-    for _ in range(iters):
-        c = _segment_means(x, _nearest(x, c), k, c)
-    return c
-
-
-def _pq_train_encode(res, s, p, train_n, iters, seed):
-    """Batched per-subspace k-means (k = 2^p) and encode.  res: (n, d) cuda."""
-    import torch
-    n, d = res.shape
-    sub = d // s
-    K = 1 << p
-    g = torch.Generator(device=res.device).manual_seed(seed)
-    tr = res[torch.randperm(n, generator=g, device=res.device)[:train_n]].reshape(-1, s, sub).transpose(0, 1)
-    c = tr[:, torch.randperm(tr.shape[1], generator=g, device=res.device)[:K]].clone()   # (s, K, sub)
-    tr = tr.contiguous()
-
-    def assign(xs):  # xs (s, m, sub) -> (s, m)
-        cn = (c * c).sum(2)
-        return (cn[:, None, :] - 2.0 * torch.bmm(xs, c.transpose(1, 2))).argmin(2)
-
-    for _ in range(iters):
-        a = torch.cat([assign(tr[:, lo:lo + 16384]) for lo in range(0, tr.shape[1], 16384)], 1)
-        c = torch.stack([_segment_means(tr[j], a[j], K, c[j]) for j in range(s)])
-    codes = torch.empty((n, s), dtype=torch.uint8, device=res.device)
-    for lo in range(0, n, 16384):
-        xs = res[lo:lo + 16384].reshape(-1, s, sub).transpose(0, 1).contiguous()
-        codes[lo:lo + 16384] = assign(xs).T.to(torch.uint8)
-    return c, codes
-
-
 def build_index_gpu(base: np.ndarray, nlist: int, s: int, p: int, seed: int = 0, train_n: int = 262_144,
                     iters: int = 12):
-    """Returns an IvfPqIndex (CSR-backed) built on cuda:0."""
-    import torch
-    from paper_2301_06672_b200.index import IvfPqIndex, PQCodebook
-    x = torch.from_numpy(base).cuda()
-    g = torch.Generator(device="cuda").manual_seed(seed)
-    tr = x[torch.randperm(x.shape[0], generator=g, device="cuda")[:max(train_n, nlist * 8)]]
-    coarse = _kmeans(tr, nlist, iters, seed)
-    assign = _nearest(x, coarse)
-    res = x - coarse[assign]
-    centers, codes = _pq_train_encode(res, s, p, min(train_n, x.shape[0]), iters, seed + 1)
-    order = torch.sort(assign, stable=True).indices
-    off = torch.zeros(nlist + 1, dtype=torch.int64, device="cuda")
-    off[1:] = torch.cumsum(torch.bincount(assign, minlength=nlist), 0)
-    idx = IvfPqIndex.from_csr(coarse.cpu().numpy(), PQCodebook(centers=centers.cpu().numpy(), p=p),
-                              off.cpu().numpy(), order.cpu().numpy(), codes[order].cpu().numpy())
-    del x, res, tr
-    torch.cuda.empty_cache()
-    return idx
+    """The product's GPU index builder (paper_2301_06672_b200.train.build_index):
+    Lloyd training on a subsample, coarse assignment + bit-exact pq_encode of
+    every row by the product kernels."""
+    from paper_2301_06672_b200.train import build_index
+    return build_index(base, nlist, s, p, seed=seed, train_n=train_n, iters=iters)
 
 
 def ground_truth_gpu(base: np.ndarray, queries: np.ndarray, k: int) -> np.ndarray:
