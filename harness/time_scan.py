@@ -22,8 +22,19 @@ def main():
     from paper_2301_06672_b200 import _lib
     from paper_2301_06672_b200.index import DeviceIndex
     cfg = W.CONFIGS[a.config]
-    base, queries = W.make_data(cfg)
-    idx = W.build_index_gpu(base, cfg["nlist"], cfg["s"], cfg["p"], seed=cfg["seed"])
+    cache = f"/tmp/ivfpq_ts_{a.config}.npz"   # same-call reuse across library variants
+    if os.path.exists(cache):
+        from paper_2301_06672_b200.index import IvfPqIndex, PQCodebook
+        z = np.load(cache)
+        idx = IvfPqIndex.from_csr(z["coarse"], PQCodebook(centers=z["centers"], p=cfg["p"]), z["off"], z["ids"],
+                                  z["codes"])
+        queries = z["queries"]
+    else:
+        base, queries = W.make_data(cfg)
+        idx = W.build_index_gpu(base, cfg["nlist"], cfg["s"], cfg["p"], seed=cfg["seed"])
+        del base
+        off, ids, codes = idx.csr()
+        np.savez(cache, coarse=idx.coarse, centers=idx.cb.centers, off=off, ids=ids, codes=codes, queries=queries)
     dev = DeviceIndex(idx, 0)
     q = torch.from_numpy(queries).cuda()
     k, P = cfg["k"], a.nprobe or cfg["nprobe"]
