@@ -543,6 +543,7 @@ int run_select(ivfpq_index* idx, const float* d_q, int64_t nq, int64_t P, uint64
 struct WsPlan {
     int G, NBUF, SD;
     size_t smem;
+    int gmem;
 };
 
 // 0 = auto (v2 when the shape fits), 1 = force v1; set by ivfpq_set_scan_kernel
@@ -567,7 +568,8 @@ bool ws_plan(const ivfpq_index* idx, int64_t P, int64_t K, int dt, WsPlan* plan)
     if (idx->p < 2 || idx->sub_d < 1 || idx->sub_d > 4 || K > WS_MAX_K) return false;
     const int64_t R = WS_R((int)N);
     const int64_t jpt = WS_JPT((int)idx->sub_d);
-    if ((idx->s_pad + R - 1) / R > jpt) return false;  // LUT rows padded to s_pad
+    // rows per builder thread beyond the TMEM budget: codebook read from global
+    const bool gmem = (idx->s_pad + R - 1) / R > jpt;
     const size_t lut_each = WsLayout((int)idx->d, (int)idx->s, (int)idx->sub_d, (int)idx->p, lut_bytes_of((int)dt), 1,
                                      2, (int)K, 2, (int)idx->s_pad).lut_each;
     int G = (int)std::max<size_t>(1, std::min<size_t>(WS_MAX_G, lut_budget_bytes() / lut_each));
@@ -588,7 +590,7 @@ bool ws_plan(const ivfpq_index* idx, int64_t P, int64_t K, int dt, WsPlan* plan)
                 const size_t sm = WsLayout((int)idx->d, (int)idx->s, (int)idx->sub_d, (int)idx->p, lut_bytes_of((int)dt),
                                            G, nb, (int)K, sd, (int)idx->s_pad).total;
                 if (sm <= SMEM_LIMIT) {
-                    *plan = WsPlan{G, nb, sd, sm};
+                    *plan = WsPlan{G, nb, sd, sm, gmem ? 1 : 0};
                     static bool printed = false;
                     if (!printed && getenv("IVFPQ_WS_PLAN_PRINT")) {
                         fprintf(stderr, "scan_ws plan: G=%d NBUF=%d SD=%d smem=%zu\n", G, nb, sd, sm);
@@ -650,6 +652,7 @@ int run_scan(ivfpq_index* idx, const float* d_q, int64_t nq, const uint64_t* d_p
         w.a = a;
         w.NBUF = plan.NBUF;
         w.SD = plan.SD;
+        w.gmem = plan.gmem;
         static const int dbg = [] {
             const char* e = getenv("IVFPQ_WS_DEBUG");
             return e ? atoi(e) : 0;

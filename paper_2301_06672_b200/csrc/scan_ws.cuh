@@ -74,6 +74,7 @@ struct WsArgs {
     int JMAX;
     int NBUF;
     int SD;                // code-block stages per scanner warp (2..WS_MAX_SD)
+    int gmem;              // 1: builders read the codebook from global memory (does not fit TMEM)
     int debug;             // perf experiments only (wrong results): bit 0 = skip LUT math, bit 1 = skip
                            // gathers + offers, bit 2 = scanners skip their blocks entirely
     int* work;             // global query counter (zeroed before launch)
@@ -347,7 +348,7 @@ struct WsLayout {
 // j = jr + R*i (jr = t / (N/4), R = 1024/N), i < jpt.  Its centers live in
 // TMEM: for owned row i, CPI columns hold c[m0..m0+3][0..SUB_D) (pairs packed
 // as (c[m0][x], c[m0+1][x]), (c[m0+2][x], c[m0+3][x])).
-template <int DT, int LOGN, int SUB_D>
+template <int DT, int LOGN, int SUB_D, bool GMEM>
 struct WsBuild {
     static constexpr int N = 1 << LOGN;
     static constexpr int NQ4 = N / 4;                                   // quads per subspace row
@@ -362,12 +363,21 @@ struct WsBuild {
 
     int u, jr;
     uint32_t tbase;  // this thread's TMEM address (lane quarter | column half)
+    // Codebooks too large for TMEM (rows per thread > JPT, e.g. cfg3 p8: 960
+    // KiB) are read per job from global memory (L2-resident) instead: gc !=
+    // nullptr.  Same packing as the TMEM columns.
+    const float* gc;
+    int s_;
 
-    __device__ void init(const float* __restrict__ centers, int s, int t, uint32_t tmem) {
+    __device__ void init(const float* __restrict__ centers, int s, int t, uint32_t tmem, bool gmem) {
         const int w = t >> 5;
         u = t % NQ4;
         jr = t / NQ4;
         tbase = tmem + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)((w >> 2) * HALF);
+        (void)gmem;
+        gc = GMEM ? centers : nullptr;
+        s_ = s;
+        if (GMEM) return;
 #pragma unroll 1
         for (int i = 0; i < JPT; ++i) {
             const int j = jr + R * i;
@@ -389,6 +399,39 @@ struct WsBuild {
         tmem_wait_st();
     }
 
+    // One owned row's centers in the TMEM column packing: r[(h*SUB_D + x)*2 + e]
+    // = c[4u + 2h + e][x] (zeros past the last subspace).
+    __device__ __forceinline__ void row(int i, uint32_t (&r)[CPI]) const {
+        if constexpr (!GMEM) {
+            tmem_ld<CPI>(tbase + i * CPI, r);
+            return;
+        }
+        const int j = jr + R * i;
+#pragma unroll
+        for (int k = 0; k < CPI; ++k) r[k] = 0u;
+        if (j < s_) {
+            // the quad's 4 x SUB_D floats are contiguous and 16-byte aligned:
+            // SUB_D vector loads (a warp reads 32 x 16 B per instruction)
+            const float4* src = reinterpret_cast<const float4*>(gc + ((size_t)j * N + 4 * u) * SUB_D);
+            float f[4 * SUB_D];
+#pragma unroll
+            for (int q = 0; q < SUB_D; ++q) {
+                const float4 v = __ldg(src + q);
+                f[4 * q + 0] = v.x;
+                f[4 * q + 1] = v.y;
+                f[4 * q + 2] = v.z;
+                f[4 * q + 3] = v.w;
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int x = 0; x < SUB_D; ++x) {
+                    r[(h * SUB_D + x) * 2 + 0] = __float_as_uint(f[(2 * h) * SUB_D + x]);
+                    r[(h * SUB_D + x) * 2 + 1] = __float_as_uint(f[(2 * h + 1) * SUB_D + x]);
+                }
+        }
+    }
+
     // The LUTs of ng lists: rq_s[g] (smem, d_pad floats) -> lut_s[g] (smem,
     // R*jpt rows of N).  Centers of row i are read from TMEM once and reused
     // for every list of the job.
@@ -402,9 +445,9 @@ struct WsBuild {
 #pragma unroll 1
         for (; i + 2 <= jpt; i += 2) {
             uint32_t c0[CPI], c1[CPI];
-            tmem_ld<CPI>(tbase + i * CPI, c0);
-            tmem_ld<CPI>(tbase + (i + 1) * CPI, c1);
-            tmem_wait_ld();
+            row(i, c0);
+            row(i + 1, c1);
+            if constexpr (!GMEM) tmem_wait_ld();
             u64 cenA[2][SUB_D], cenB[2][SUB_D];
 #pragma unroll
             for (int h = 0; h < 2; ++h)
@@ -423,8 +466,8 @@ struct WsBuild {
         }
         if (i < jpt) {
             uint32_t c[CPI];
-            tmem_ld<CPI>(tbase + i * CPI, c);
-            tmem_wait_ld();
+            row(i, c);
+            if constexpr (!GMEM) tmem_wait_ld();
             u64 cen[2][SUB_D];
 #pragma unroll
             for (int h = 0; h < 2; ++h)
@@ -1043,7 +1086,7 @@ __global__ void __launch_bounds__(256) ws_plan_kernel(const ScanArgs a, int G, i
 }
 #endif
 
-template <int DT, int LOGN, int SUB_D>
+template <int DT, int LOGN, int SUB_D, bool GMEM>
 __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) {
     using T = typename LutTraits<DT>::T;
     extern __shared__ __align__(1024) uint8_t ws_smem[];
@@ -1054,7 +1097,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
     const WsLayout L(a.d, a.s, SUB_D, LOGN, (int)sizeof(T), G, NBUF, K, SD, a.s_pad);
     const size_t lut_each = L.lut_each;
     const int d_pad = (int)L.d_pad;
-    const int jpt = (a.s_pad + WsBuild<DT, LOGN, SUB_D>::R - 1) / WsBuild<DT, LOGN, SUB_D>::R;  // rows per builder
+    const int jpt = (a.s_pad + WsBuild<DT, LOGN, SUB_D, GMEM>::R - 1) / WsBuild<DT, LOGN, SUB_D, GMEM>::R;  // rows per builder
     u64* pfull = reinterpret_cast<u64*>(smem + L.bars);  // pfull[PD]: job + residuals prepared
     u64* pempty = pfull + WS_PD;                          // pempty[PD]: prep entry consumed
     u64* full = pempty + WS_PD;                           // full[NBUF]: LUTs ready
@@ -1079,7 +1122,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
         S->cur = 0;
         S->q = -1;
     }
-    using Builder = WsBuild<DT, LOGN, SUB_D>;
+    using Builder = WsBuild<DT, LOGN, SUB_D, GMEM>;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.tmem);
     if (warp == 0) tmem_alloc<Builder::NCOL>(smem_addr(tmem_slot));
     if (threadIdx.x == 0) {
@@ -1154,7 +1197,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
         // =========================== builders ===========================
         const int t = threadIdx.x;
         Builder B;
-        B.init(a.centers, a.s, t, tmem);
+        B.init(a.centers, a.s, t, tmem, w.gmem != 0);
         const uint32_t prq_s = smem_addr(prq), lut_s = smem_addr(lut_all);
         int slot = 0, eph = 0;  // LUT slot of this job, parity of its previous release
         bool wrapped = false;

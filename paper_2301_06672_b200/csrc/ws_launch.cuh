@@ -7,18 +7,26 @@
 
 namespace ivfpq {
 
-template <int DT, int LOGN, int SUB_D>
-cudaError_t ws_launch_t(const WsArgs& w, size_t smem, int grid, cudaStream_t st) {
+template <int DT, int LOGN, int SUB_D, bool GMEM>
+cudaError_t ws_launch_g(const WsArgs& w, size_t smem, int grid, cudaStream_t st) {
     static int ok = -1;
     if (ok < 0) {
-        cudaError_t e = cudaFuncSetAttribute(scan_ws_kernel<DT, LOGN, SUB_D>,
+        cudaError_t e = cudaFuncSetAttribute(scan_ws_kernel<DT, LOGN, SUB_D, GMEM>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         if (e != cudaSuccess) return e;
         ok = 1;
     }
     if (!ok) return cudaErrorNotSupported;
-    scan_ws_kernel<DT, LOGN, SUB_D><<<grid, WS_THREADS, smem, st>>>(w);
+    scan_ws_kernel<DT, LOGN, SUB_D, GMEM><<<grid, WS_THREADS, smem, st>>>(w);
     return cudaGetLastError();
+}
+
+// GMEM: the builders read the codebook from global memory (it does not fit
+// TMEM); a separate instantiation keeps the common TMEM kernel's code as is.
+template <int DT, int LOGN, int SUB_D>
+cudaError_t ws_launch_t(const WsArgs& w, size_t smem, int grid, cudaStream_t st) {
+    return w.gmem ? ws_launch_g<DT, LOGN, SUB_D, true>(w, smem, grid, st)
+                  : ws_launch_g<DT, LOGN, SUB_D, false>(w, smem, grid, st);
 }
 
 template <int DT, int LOGN>

@@ -192,6 +192,7 @@ def _random_index(rng, n, d, s, p, nlist, empty_lists=()):
     dict(n=20000, d=96, s=32, p=8, nlist=32, P=6, k=10),         # cfg5 shape (sub_d = 3)
     dict(n=8000, d=120, s=24, p=5, nlist=16, P=4, k=10),         # p=5, s not a multiple of 16
     dict(n=5000, d=40, s=20, p=4, nlist=8, P=8, k=64),           # p=4, nprobe = nlist
+    dict(n=6000, d=480, s=120, p=8, nlist=16, P=4, k=10),        # codebook beyond TMEM: builders read it from L2
 ])
 def test_search_batch_vs_c_oracle_random(pkg, shape, scan_kernel):
     from oracle import c_oracle
