@@ -583,7 +583,9 @@ bool ws_plan(const ivfpq_index* idx, int64_t P, int64_t K, int dt, WsPlan* plan)
     // (fp8: G=3 x 3 slots, 4.86 ms vs G=4 x 2 slots, 5.18 ms), then code
     // stages; otherwise 2 slots (f16: G=2 x 2, 6.33 ms vs G=1 x 4, 7.38 ms).
     const int G0 = G;
-    for (int min_nb = 3; min_nb >= 2; --min_nb)
+    // (a single slot -- build, then scan -- is the last resort before the
+    // per-query kernel: cfg3 p8 with f16 LUTs of 120 KiB)
+    for (int min_nb = 3; min_nb >= 1; --min_nb)
     for (G = G0; G >= (min_nb == 3 ? 2 : 1); --G)
         for (int sd = 0; sd <= 0; ++sd)  // codes go L2 -> registers: no smem stages
             for (int nb = env_nb ? env_nb : WS_MAX_NBUF; nb >= min_nb; --nb) {

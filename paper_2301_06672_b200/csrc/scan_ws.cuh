@@ -900,7 +900,9 @@ __device__ void ws_scanner(const ScanArgs& a, WsJob* jobs, int* cnt, u64* full, 
         if (!hn) {
             const int ns = slot + 1 == NBUF ? 0 : slot + 1;
             const int nph = slot + 1 == NBUF ? ph ^ 1 : ph;
-            if (mbar_test(full + ns, (uint32_t)nph) && jobs[ns].qs >= 0) {
+            // (NBUF = 1: the "next" slot is this one; its previous phase would
+            // test as complete, so there is no cross-job prefetch)
+            if (NBUF > 1 && mbar_test(full + ns, (uint32_t)nph) && jobs[ns].qs >= 0) {
                 nt.load(jobs + ns, lane);
                 hn = ws_grab(nt, cnt, ns, lut_s0 + (uint32_t)ns * slot_bytes, lut_each, lane, nxt);
                 cross = true;  // (an empty next job is left to the blocking path)
