@@ -383,7 +383,7 @@ def cpu_baseline(idx, queries, gt, k, P, prec, n_sample):
     from harness.cpu_baseline import CpuBaseline
     from harness.workload import recall_at
     cb = CpuBaseline(idx)
-    n = n_sample or min(queries.shape[0], max(64, 40 * cb.workers))
+    n = n_sample or cb.size_for(queries, k, P, prec, seconds=10.0)
     qps, ids, wall = cb.run(queries[:n], k, P, prec)
     cb.close()
     return {"value": round(qps, 2), "unit": "queries/s", "cores": cb.workers, "kind": "port",
@@ -405,17 +405,18 @@ def run_reference(args, rank, world):
     P = args.nprobe or cfg["nprobe"]
     k = cfg["k"]
     cb = CpuBaseline(idx)
-    n = args.cpu_sample or min(queries.shape[0], max(32, 25 * cb.workers))
+    # each step is a bounded sample sized so the whole run is ~90 s of host time
+    n = args.cpu_sample or cb.size_for(queries, k, P, args.dtype, seconds=90.0 / (args.warmup + args.steps))
     nq = queries.shape[0]
     total_q, total_t, rec = 0, 0.0, []
     for i in range(args.warmup + args.steps):
-        lo = (i * n) % nq
-        sample = queries[lo:lo + n]
+        rows = (i * n + np.arange(n)) % nq
+        sample = queries[rows]
         qps, ids, wall = cb.run(sample, k, P, args.dtype)
         if i >= args.warmup:
             total_q += sample.shape[0]
             total_t += wall
-            rec.append(recall_at(ids[:, :10], gt[lo:lo + n]))
+            rec.append(recall_at(ids[:, :10], gt[rows]))
     cb.close()
     value = total_q / total_t
     line = {"metric": METRIC, "value": round(value, 2), "unit": "queries/s", "n_gpus": world, "steps": args.steps,

@@ -66,6 +66,13 @@ class CpuBaseline:
         ids = np.concatenate([r[0] for r in res])
         return queries.shape[0] / wall, ids, wall
 
+    def size_for(self, queries: np.ndarray, k: int, nprobe: int, prec: str, seconds: float) -> int:
+        """Query count that takes about `seconds` of wall time, from a short
+        pilot run (4 queries per worker); clamped to [workers, len(queries)]."""
+        pilot = queries[:4 * self.workers]
+        qps, _, _ = self.run(pilot, k, nprobe, prec)
+        return int(min(queries.shape[0], max(self.workers, qps * seconds)))
+
     def close(self):
         self.pool.terminate()
         self.tmp.cleanup()
