@@ -119,7 +119,7 @@ struct ivfpq_index {
     cudaStream_t stream = nullptr;
     std::mutex mu;
     // scratch
-    DevBuf q, dist, pkeys, oids, odist, oshort, keys, ncand, work, plan_jobs, plan_rq, plan_nj, plan_nc, tc_sl, flags;
+    DevBuf q, dist, pkeys, oids, odist, oshort, keys, ncand, work, plan_jobs, plan_rq, plan_nj, plan_nc, tc_sl, flags, glut;
     int num_sms = 0;
 };
 
@@ -297,28 +297,28 @@ __global__ void topk_hook_kernel(const int64_t* ids, const float* dists, int n, 
 
 // ---- dispatch -------------------------------------------------------------------
 template <int DT, int LOGN>
-int launch_scan_t(const ScanArgs& a, size_t smem, cudaStream_t st) {
+int launch_scan_t(const ScanArgs& a, size_t smem, void* glut, int grid, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
         CK(cudaFuncSetAttribute(scan_kernel<DT, LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_LIMIT));
         attr = true;
     }
-    scan_kernel<DT, LOGN><<<a.nq, TK_BLOCK, smem, st>>>(a);
+    scan_kernel<DT, LOGN><<<grid, TK_BLOCK, smem, st>>>(a, glut);
     KCHECK();
     return IVFPQ_OK;
 }
 
 template <int DT>
-int launch_scan_dt(int logn, const ScanArgs& a, size_t smem, cudaStream_t st) {
+int launch_scan_dt(int logn, const ScanArgs& a, size_t smem, void* glut, int grid, cudaStream_t st) {
     switch (logn) {
-        case 1: return launch_scan_t<DT, 1>(a, smem, st);
-        case 2: return launch_scan_t<DT, 2>(a, smem, st);
-        case 3: return launch_scan_t<DT, 3>(a, smem, st);
-        case 4: return launch_scan_t<DT, 4>(a, smem, st);
-        case 5: return launch_scan_t<DT, 5>(a, smem, st);
-        case 6: return launch_scan_t<DT, 6>(a, smem, st);
-        case 7: return launch_scan_t<DT, 7>(a, smem, st);
-        case 8: return launch_scan_t<DT, 8>(a, smem, st);
+        case 1: return launch_scan_t<DT, 1>(a, smem, glut, grid, st);
+        case 2: return launch_scan_t<DT, 2>(a, smem, glut, grid, st);
+        case 3: return launch_scan_t<DT, 3>(a, smem, glut, grid, st);
+        case 4: return launch_scan_t<DT, 4>(a, smem, glut, grid, st);
+        case 5: return launch_scan_t<DT, 5>(a, smem, glut, grid, st);
+        case 6: return launch_scan_t<DT, 6>(a, smem, glut, grid, st);
+        case 7: return launch_scan_t<DT, 7>(a, smem, glut, grid, st);
+        case 8: return launch_scan_t<DT, 8>(a, smem, glut, grid, st);
     }
     return set_err(IVFPQ_EINVAL, "pq_bits %d out of range 1..8", logn);
 }
@@ -611,13 +611,24 @@ int run_scan(ivfpq_index* idx, const float* d_q, int64_t nq, const uint64_t* d_p
     CKR(check_dtype(dt));
     const size_t lut_each = (size_t)(idx->s << idx->p) * lut_bytes_of(dt);
     const size_t fixed = ScanSmemLayout((int)idx->d, 1, 0, (int)K).total;
-    if (fixed + lut_each > SMEM_LIMIT)
-        return set_err(IVFPQ_EUNSUPPORTED, "LUT of %zu bytes (s=%lld, p=%lld, dtype %d) does not fit shared memory",
-                       lut_each, (long long)idx->s, (long long)idx->p, dt);
-    int G = (int)std::max<size_t>(1, std::min<size_t>(SCAN_MAX_G, lut_budget_bytes() / lut_each));
+    if (fixed > SMEM_LIMIT)
+        return set_err(IVFPQ_EUNSUPPORTED, "d=%lld, k=%lld: scan state does not fit shared memory", (long long)idx->d,
+                       (long long)K);
+    // A table larger than shared memory (f32 LUT at s=240, p=8) is built in a
+    // per-block global scratch; the per-query kernel then strides over the
+    // queries with a bounded grid.  (Only reachable when v2 cannot plan it.)
+    const bool glut = fixed + lut_each > SMEM_LIMIT;
+    int G = glut ? 1 : (int)std::max<size_t>(1, std::min<size_t>(SCAN_MAX_G, lut_budget_bytes() / lut_each));
     G = (int)std::min<int64_t>(G, std::max<int64_t>(1, P));
     while (G > 1 && ScanSmemLayout((int)idx->d, G, lut_each, (int)K).total > SMEM_LIMIT) --G;
-    const size_t smem = ScanSmemLayout((int)idx->d, G, lut_each, (int)K).total;
+    const size_t smem = ScanSmemLayout((int)idx->d, G, glut ? 0 : lut_each, (int)K).total;
+    int grid = (int)std::max<int64_t>(nq, 1);
+    void* glut_p = nullptr;
+    if (glut) {
+        grid = (int)std::min<int64_t>(grid, (int64_t)std::max(idx->num_sms, 1) * 4);
+        CKR(idx->glut.ensure((size_t)grid * lut_each));
+        glut_p = idx->glut.p;
+    }
     ScanArgs a;
     a.queries = d_q;
     a.probes = d_pk;
@@ -709,7 +720,7 @@ int run_scan(ivfpq_index* idx, const float* d_q, int64_t nq, const uint64_t* d_p
             return set_err(IVFPQ_ECUDA, "scan_ws launch failed: %s", cudaGetErrorString(e));
         a.G = G;  // register budget not met by this build: per-query kernel
     }
-    return DISPATCH_DT_LOGN(dt, (int)idx->p, launch_scan_dt, a, smem, st);
+    return DISPATCH_DT_LOGN(dt, (int)idx->p, launch_scan_dt, a, smem, glut_p, grid, st);
 }
 
 int validate_search(ivfpq_index* idx, int64_t nq, int64_t k, int64_t nprobe, int dt) {
@@ -922,7 +933,7 @@ int ivfpq_index_destroy(ivfpq_index* idx) {
                     idx->tc_img};
     for (void* ptr : ptrs)
         if (ptr) cudaFree(ptr);
-    for (DevBuf* b : {&idx->q, &idx->dist, &idx->pkeys, &idx->oids, &idx->odist, &idx->oshort, &idx->keys, &idx->ncand,
+    for (DevBuf* b : {&idx->glut, &idx->q, &idx->dist, &idx->pkeys, &idx->oids, &idx->odist, &idx->oshort, &idx->keys, &idx->ncand,
                       &idx->work, &idx->plan_jobs, &idx->plan_rq, &idx->plan_nj, &idx->plan_nc, &idx->tc_sl,
                       &idx->flags})
         b->release();

@@ -153,11 +153,13 @@ struct ScanSmemLayout {
 };
 
 template <int DT, int LOGN>
-__global__ void __launch_bounds__(TK_BLOCK) scan_kernel(const ScanArgs a) {
+// glut: null = LUTs in shared memory; else a per-block global LUT scratch
+// [gridDim.x][G][s << p] for tables larger than shared memory.
+__global__ void __launch_bounds__(TK_BLOCK) scan_kernel(const ScanArgs a, void* glut) {
     using T = typename LutTraits<DT>::T;
     extern __shared__ __align__(16) uint8_t smem[];
     const int lut_elems = a.s << LOGN;
-    const ScanSmemLayout lay(a.d, a.G, (size_t)lut_elems * sizeof(T), a.K);
+    const ScanSmemLayout lay(a.d, a.G, glut ? 0 : (size_t)lut_elems * sizeof(T), a.K);
     float* qv = reinterpret_cast<float*>(smem + lay.q);
     float* rq = reinterpret_cast<float*>(smem + lay.rq);
     int* g_pref = reinterpret_cast<int*>(smem + lay.grp);       // [G+1]
@@ -165,11 +167,16 @@ __global__ void __launch_bounds__(TK_BLOCK) scan_kernel(const ScanArgs a) {
     int* g_lc = g_len + SCAN_MAX_G;                              // [G]
     int* g_n = g_lc + SCAN_MAX_G;                                // [1]
     long long* g_off = reinterpret_cast<long long*>(smem + lay.grp + 128);  // [G]
-    T* lut = reinterpret_cast<T*>(smem + lay.lut);
+    // Tables beyond shared memory (f32 LUT at s=240, p=8: 240 KiB) live in
+    // this block's slice of a global scratch (L1/L2-resident; generic loads),
+    // and the grid strides over the queries so the scratch stays bounded.
+    T* lut = glut ? reinterpret_cast<T*>(glut) + (size_t)blockIdx.x * a.G * lut_elems
+                    : reinterpret_cast<T*>(smem + lay.lut);
     BlockTopK tk;
     tk.bind(smem + lay.tk, a.K);
 
-    const int qi = blockIdx.x;
+    for (int qi = blockIdx.x; qi < a.nq; qi += gridDim.x) {
+    __syncthreads();  // the previous query's results were read from tk
     for (int t = threadIdx.x; t < a.d; t += blockDim.x) qv[t] = a.queries[(size_t)qi * a.d + t];
     tk.init();
 
@@ -258,6 +265,7 @@ __global__ void __launch_bounds__(TK_BLOCK) scan_kernel(const ScanArgs a) {
         }
         if (threadIdx.x == 0) a.out_short[qi] = ncand < a.K ? 1 : 0;
     }
+    }  // queries
 }
 
 }  // namespace ivfpq

@@ -193,6 +193,7 @@ def _random_index(rng, n, d, s, p, nlist, empty_lists=()):
     dict(n=8000, d=120, s=24, p=5, nlist=16, P=4, k=10),         # p=5, s not a multiple of 16
     dict(n=5000, d=40, s=20, p=4, nlist=8, P=8, k=64),           # p=4, nprobe = nlist
     dict(n=6000, d=480, s=120, p=8, nlist=16, P=4, k=10),        # codebook beyond TMEM: builders read it from L2
+    dict(n=4000, d=240, s=240, p=8, nlist=16, P=4, k=10),        # f32 LUT of 240 KiB > smem: global-scratch LUT
 ])
 def test_search_batch_vs_c_oracle_random(pkg, shape, scan_kernel):
     from oracle import c_oracle
