@@ -231,14 +231,16 @@ __global__ void decode_kernel(const typename LutTraits<DT>::T* __restrict__ in, 
 // build_lut hook: the same device routine the search kernel uses (ng = 1).
 template <int DT, int LOGN>
 __global__ void __launch_bounds__(TK_BLOCK) build_lut_kernel(const float* centers, int s, int sub_d, const float* rq_g,
-                                                             typename LutTraits<DT>::T* out) {
+                                                             typename LutTraits<DT>::T* out, int direct) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int d = s * sub_d;
     float* rq = reinterpret_cast<float*>(smem);
-    auto* lut = reinterpret_cast<typename LutTraits<DT>::T*>(smem + (((size_t)d * 4 + 15) & ~(size_t)15));
+    // direct: a table larger than shared memory is written straight to `out`
+    auto* lut = direct ? out : reinterpret_cast<typename LutTraits<DT>::T*>(smem + (((size_t)d * 4 + 15) & ~(size_t)15));
     for (int t = threadIdx.x; t < d; t += blockDim.x) rq[t] = rq_g[t];
     __syncthreads();
     build_luts<DT, LOGN>(lut, s << LOGN, centers, rq, d, sub_d, 1);
+    if (direct) return;
     __syncthreads();
     for (int e = threadIdx.x; e < (s << LOGN); e += blockDim.x) out[e] = lut[e];
 }
@@ -247,13 +249,17 @@ __global__ void __launch_bounds__(TK_BLOCK) build_lut_kernel(const float* center
 // -- the same lookup16 / lut_widen / lut_finish arithmetic as the search kernel.
 template <int DT, int LOGN>
 __global__ void __launch_bounds__(TK_BLOCK) scan_list_kernel(const uint8_t* codes, int64_t L, int s, const void* entries,
-                                                             float* out) {
+                                                             float* out, int direct) {
     using T = typename LutTraits<DT>::T;
     extern __shared__ __align__(16) uint8_t smem[];
-    T* lut = reinterpret_cast<T*>(smem);
     const T* g = reinterpret_cast<const T*>(entries);
-    for (int e = threadIdx.x; e < (s << LOGN); e += blockDim.x) lut[e] = g[e];
-    __syncthreads();
+    // direct: a table larger than shared memory is gathered from global memory
+    T* st = reinterpret_cast<T*>(smem);
+    if (!direct) {
+        for (int e = threadIdx.x; e < (s << LOGN); e += blockDim.x) st[e] = g[e];
+        __syncthreads();
+    }
+    const T* lut = direct ? g : st;
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < L; v += (int64_t)gridDim.x * blockDim.x) {
         const uint8_t* row = codes + v * s;
         float acc = 0.0f;
@@ -1113,7 +1119,8 @@ int build_lut_dt(int logn, const float* dc, int s, int sub_d, const float* drq, 
 #define BL(L)                                                                                          \
     case L:                                                                                            \
         CKR(set_smem_attr((const void*)build_lut_kernel<DT, L>, SMEM_LIMIT));                           \
-        build_lut_kernel<DT, L><<<1, TK_BLOCK, smem>>>(dc, s, sub_d, drq, reinterpret_cast<T*>(dout)); \
+        build_lut_kernel<DT, L><<<1, TK_BLOCK, smem > SMEM_LIMIT ? ((size_t)s * sub_d * 4 + 15) & ~(size_t)15 : smem>>>( \
+            dc, s, sub_d, drq, reinterpret_cast<T*>(dout), smem > SMEM_LIMIT); \
         break;
         BL(1) BL(2) BL(3) BL(4) BL(5) BL(6) BL(7) BL(8)
 #undef BL
@@ -1129,7 +1136,8 @@ int scan_list_dt(int logn, const uint8_t* dcodes, int64_t L, int s, const void* 
 #define SL(LG)                                                                                  \
     case LG:                                                                                    \
         CKR(set_smem_attr((const void*)scan_list_kernel<DT, LG>, SMEM_LIMIT));                   \
-        scan_list_kernel<DT, LG><<<grid, TK_BLOCK, smem>>>(dcodes, L, s, dent, dout);           \
+        scan_list_kernel<DT, LG><<<grid, TK_BLOCK, smem > SMEM_LIMIT ? 0 : smem>>>(dcodes, L, s, dent, dout, \
+                                                                                smem > SMEM_LIMIT);     \
         break;
         SL(1) SL(2) SL(3) SL(4) SL(5) SL(6) SL(7) SL(8)
 #undef SL
@@ -1149,7 +1157,6 @@ int ivfpq_build_lut(const float* centers, int64_t s, int64_t p, int64_t sub_d, c
     const int64_t d = s * sub_d, ne = s << p;
     const size_t eb = lut_bytes_of(dt);
     const size_t smem = (((size_t)d * 4 + 15) & ~(size_t)15) + ne * eb;
-    if (smem > SMEM_LIMIT) return set_err(IVFPQ_EUNSUPPORTED, "LUT does not fit shared memory");
     Tmp<float> dc, drq;
     Tmp<uint8_t> dout;
     CK(dc.alloc(ne * sub_d));
@@ -1167,7 +1174,6 @@ int ivfpq_scan_list(const uint8_t* codes, int64_t L, int64_t s, int64_t p, const
     if (s < 1 || p < 1 || p > 8 || L < 0) return set_err(IVFPQ_EINVAL, "invalid scan shape");
     const int64_t ne = s << p;
     const size_t eb = lut_bytes_of(dt);
-    if ((size_t)ne * eb > SMEM_LIMIT) return set_err(IVFPQ_EUNSUPPORTED, "LUT does not fit shared memory");
     if (L == 0) return IVFPQ_OK;
     for (int64_t i = 0; i < L * s; ++i)
         if (codes[i] >= (1 << p)) return set_err(IVFPQ_EINVAL, "code byte out of range for the table");

@@ -98,6 +98,22 @@ def test_build_lut_and_scan_bit_exact(pkg, name):
             assert np.array_equal(r, c[f"scan_{prec}_{n}"]), (name, n, prec)
 
 
+def test_build_lut_and_scan_hooks_beyond_smem(pkg):
+    """s=240, p=8 (cfg3 shape): the f32 table is 240 KiB > shared memory, so the
+    hooks build / gather it in global memory; bit-exact vs the C oracle."""
+    from oracle import c_oracle
+    rng = np.random.default_rng(240)
+    cb = pkg.PQCodebook(centers=(rng.standard_normal((240, 256, 4)) * 0.3).astype(np.float32), p=8)
+    rq = (rng.standard_normal(960) * 0.3).astype(np.float32)
+    codes = rng.integers(0, 256, (700, 240)).astype(np.uint8)
+    ids = np.arange(700, dtype=np.int64)
+    for prec in PRECS:
+        lut = pkg.build_lut(cb, rq, prec)
+        assert np.array_equal(lut.entries, c_oracle.build_lut(cb.centers, rq, prec)), prec
+        _, r = pkg.scan_list(ids, codes, lut)
+        assert np.array_equal(r, c_oracle.scan(codes, lut.entries, prec)), prec
+
+
 def test_build_lut_p6_codebook(pkg):
     z = np.load(os.path.join(GOLDEN, "codebook_p6.npz"))
     cb = pkg.PQCodebook(centers=z["centers"], p=6)
