@@ -53,7 +53,10 @@ __host__ __device__ constexpr int WS_JPT(int sub_d) { return 64 / (sub_d * WS_BW
 constexpr int WS_THREADS = (WS_BW + WS_SW + 1) * 32;
 constexpr int WS_MAX_G = 8;
 constexpr int WS_MAX_NBUF = 6;
-constexpr int WS_NQS = 4;                    // per-query states (query top-k lists) in flight
+#ifndef WS_NQS_CFG
+#define WS_NQS_CFG 4
+#endif
+constexpr int WS_NQS = WS_NQS_CFG;           // per-query states (query top-k lists) in flight
 constexpr int WS_PD = 8;                     // prep ring depth (jobs prepared ahead)
 constexpr int WS_MAX_SD = 3;                 // code-block stages per scanner warp
 #ifndef WS_WBUF_CFG
