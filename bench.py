@@ -383,7 +383,7 @@ def cpu_baseline(idx, queries, gt, k, P, prec, n_sample):
     from harness.cpu_baseline import CpuBaseline
     from harness.workload import recall_at
     cb = CpuBaseline(idx)
-    n = n_sample or cb.size_for(queries, k, P, prec, seconds=10.0)
+    n = n_sample or cb.size_for(queries, k, P, prec, seconds=20.0)  # pilot underestimates QPS ~2x
     qps, ids, wall = cb.run(queries[:n], k, P, prec)
     cb.close()
     return {"value": round(qps, 2), "unit": "queries/s", "cores": cb.workers, "kind": "port",
