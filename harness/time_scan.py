@@ -57,28 +57,7 @@ def main():
             e1.synchronize()
             if r:
                 ts.append(e0.elapsed_time(e1))
-        print(f"{a.config} {prec} nprobe {P}: scan {np.mean(ts):.3f} ms (min {np.min(ts):.3f})",
-              f"debug={os.environ.get('IVFPQ_WS_DEBUG', '0')}", flush=True)
-        if int(os.environ.get("IVFPQ_WS_DEBUG", "0")) & 32:
-            dump_prof()
-
-
-
-def dump_prof(nsm=148):
-    """Per-role cycle summary after a run with IVFPQ_WS_DEBUG bit 5."""
-    import ctypes
-    import numpy as np
-    from paper_2301_06672_b200 import _lib
-    buf = np.zeros((nsm, 32, 8), dtype=np.uint64)
-    fn = _lib.lib.ivfpq_debug_ws_prof
-    fn.argtypes = [ctypes.c_void_p, ctypes.c_int64]
-    _lib.check(fn(buf.ctypes.data, buf.nbytes))
-    b = buf.astype(np.float64) / 1e6
-    bw, sw = int(os.environ.get("WS_BW", "8")), int(os.environ.get("WS_SW", "11"))  # WS_BW_CFG / WS_SW_CFG
-    roles = {"builders": range(0, bw), "scanners": range(bw, bw + sw), "prep": [bw + sw]}
-    for name, ws in roles.items():
-        m = b[:, list(ws), :].mean(axis=(0, 1))
-        print(f"  {name:9s} Mcycles/warp: " + " ".join(f"{x:7.3f}" for x in m))
+        print(f"{a.config} {prec} nprobe {P}: scan {np.mean(ts):.3f} ms (min {np.min(ts):.3f})", flush=True)
 
 
 if __name__ == "__main__":

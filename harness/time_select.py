@@ -44,22 +44,7 @@ def main():
             ts.append(e0.elapsed_time(e1))
     n = _lib.ctypes.c_int64()
     _lib.check(_lib.lib.ivfpq_debug_select_flagged(dev.handle, _lib.ctypes.byref(n)))
-    print(f"{a.config} select nprobe {P} mode {a.mode}: {np.mean(ts):.3f} ms  flagged={n.value}"
-          f"  IVFPQ_TC_DEBUG={os.environ.get('IVFPQ_TC_DEBUG', '0')}")
-    if int(os.environ.get("IVFPQ_TC_DEBUG", "0")) & 4:
-        nb = (q.shape[0] + 127) // 128
-        buf = np.zeros(nb * 16, np.uint64)
-        _lib.lib.ivfpq_debug_ws_prof.argtypes = [_lib.ctypes.c_void_p, _lib.ctypes.c_int64]
-        _lib.check(_lib.lib.ivfpq_debug_ws_prof(buf.ctypes.data, buf.nbytes))
-        b = buf.reshape(nb, 16)
-        g0, g1 = b[:, 8].astype(np.int64), b[:, 9].astype(np.int64)
-        t0 = g0.min()
-        print("  CTA start (us):", np.round(np.sort(g0 - t0) / 1e3, 1)[::8].tolist())
-        print("  CTA end (us):", np.round(np.sort(g1 - t0) / 1e3, 1)[::8].tolist() + [round(float((g1 - t0).max()) / 1e3, 1)], " distinct SMs:", len(set(b[:, 10].tolist())))
-        m = b[:, :8].astype(np.float64).mean(0)
-        names = ["prod_wait_empty", "prod_total", "mma_wait_acce", "mma_wait_full", "mma_total", "epi_wait_accf",
-                 "epi_total", "setup"]
-        print("  " + "  ".join(f"{k}={v / 1e3:.1f}K" for k, v in zip(names, m)))
+    print(f"{a.config} select nprobe {P} mode {a.mode}: {np.mean(ts):.3f} ms  flagged={n.value}")
 
 
 if __name__ == "__main__":

@@ -61,8 +61,6 @@ struct CoarseTcArgs {
     int32_t* ncand;          // [nslices][nq] count (TC_CAP + 1 = overflow)
     float* thr;              // [nslices][nq]
     int nq, nc, d, tiles_per_slice, nkc;
-    int debug;                            // 1: no epilogue work, 2: copy each stage once, 4: timers
-    unsigned long long* prof;             // [gridDim][8] cycle counters (debug & 4)
 };
 
 struct CoarseRerankArgs {
@@ -242,9 +240,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) coarse_tc_kernel(const CoarseTc
     const int t_end = min(ntiles_total, t_begin + a.tiles_per_slice);
     const int ntl = max(0, t_end - t_begin);
     const int nsteps = 2 * ntl;  // pass 1 then pass 2 over the same tiles
-    const long long t_start = clock64();
-    unsigned long long g_start;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
 
     // ---- setup: barriers, TMEM (2 accumulators x 128 columns + A)
     if (threadIdx.x < TC_M) cnt[threadIdx.x] = 0;
@@ -268,37 +263,25 @@ __global__ void __launch_bounds__(TC_THREADS, 1) coarse_tc_kernel(const CoarseTc
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
-    if ((a.debug & 4) && threadIdx.x == 0) a.prof[blockIdx.y * 16 + 7] = clock64() - t_start;  // setup
 
     if (warp == 0) {
         // ---- producer: centroid tile images through the stage ring (both passes)
         if (lane == 0) {
-            long long wait_cyc = 0, t_all = clock64();
             int s = 0;
             uint32_t ph = 0;
             int it = 0;
             for (int st = 0; st < nsteps; ++st) {
                 const int t = st < ntl ? st : st - ntl;
                 for (int kc = 0; kc < nkc; ++kc, ++it) {
-                    const long long t0 = clock64();
                     if (it >= TC_STAGES) tc_mbar_wait(empty + s, ph ^ 1);
-                    wait_cyc += clock64() - t0;
-                    if ((a.debug & 2) && it >= TC_STAGES) {
-                        tc_mbar_arrive(full + s);
-                    } else {
                     tc_expect_tx(full + s, TC_N * 128);
                     tc_bulk(tc_smem(sB + (size_t)s * TC_N * 128),
                             a.cimg + ((size_t)(t_begin + t) * nkc + kc) * (TC_N * 32), TC_N * 128, full + s);
-                    }
                     if (++s == TC_STAGES) {
                         s = 0;
                         ph ^= 1;
                     }
                 }
-            }
-            if (a.debug & 4) {
-                a.prof[blockIdx.y * 16 + 0] = wait_cyc;
-                a.prof[blockIdx.y * 16 + 1] = clock64() - t_all;
             }
         }
     } else if (warp == 1) {
@@ -308,19 +291,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) coarse_tc_kernel(const CoarseTc
                                        ((uint32_t)(TC_M >> 4) << 24);
             int s = 0;
             uint32_t ph = 0;
-            long long w_acc = 0, w_full = 0, t_all = clock64();
             tc_mbar_wait(aready, 0);
             for (int st = 0; st < nsteps; ++st) {
                 const int ab = st & 1;
-                long long t0 = clock64();
                 if (st >= 2) tc_mbar_wait(acce + ab, ((st >> 1) - 1) & 1);
-                w_acc += clock64() - t0;
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t dcol = tmem + (uint32_t)(ab * TC_N);
                 for (int kc = 0; kc < nkc; ++kc) {
-                    t0 = clock64();
                     tc_mbar_wait(full + s, ph);
-                    w_full += clock64() - t0;
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                     const uint32_t b0 = tc_smem(sB + (size_t)s * TC_N * 128);
 #pragma unroll
@@ -334,11 +312,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) coarse_tc_kernel(const CoarseTc
                     }
                 }
                 tc_commit(accf + ab);  // accumulator ready
-            }
-            if (a.debug & 4) {
-                a.prof[blockIdx.y * 16 + 2] = w_acc;
-                a.prof[blockIdx.y * 16 + 3] = w_full;
-                a.prof[blockIdx.y * 16 + 4] = clock64() - t_all;
             }
         }
     } else if (warp >= 4) {
@@ -371,7 +344,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) coarse_tc_kernel(const CoarseTc
 #pragma unroll
         for (int g = 0; g < 32; ++g) gmin[g] = __int_as_float(0x7f800000);
         float thr = __int_as_float(0x7f800000);
-        long long w_af = 0, t_all = clock64();
         for (int st = 0; st < nsteps; ++st) {
             const int ab = st & 1;
             const bool pass2 = st >= ntl;
@@ -388,15 +360,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) coarse_tc_kernel(const CoarseTc
                 if (q0 + r >= a.nq) thr = -__int_as_float(0x7f800000);  // padding row: nominate nothing
                 asm volatile("bar.sync 1, %0;" ::"n"(32 * TC_EPI) : "memory");
             }
-            const long long t0 = clock64();
             tc_mbar_wait(accf + ab, (st >> 1) & 1);
-            w_af += clock64() - t0;
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            if (a.debug & 1) {
-                __syncwarp();
-                if (lane == 0) tc_mbar_arrive(acce + ab);
-                continue;
-            }
             uint32_t v0[32], v1[32];
             const uint32_t col = tmem + lane_base + (uint32_t)(ab * TC_N + 64 * h);
             tc_ld32(col, v0);
@@ -430,10 +395,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) coarse_tc_kernel(const CoarseTc
                 }
             }
         }
-        if ((a.debug & 4) && threadIdx.x == 128) {
-            a.prof[blockIdx.y * 16 + 5] = w_af;
-            a.prof[blockIdx.y * 16 + 6] = clock64() - t_all;
-        }
         asm volatile("bar.sync 1, %0;" ::"n"(32 * TC_EPI) : "memory");
         if (h == 0 && q0 + r < a.nq) {
             const size_t row = (size_t)blockIdx.x * a.nq + q0 + r;
@@ -448,15 +409,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) coarse_tc_kernel(const CoarseTc
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
-    if ((a.debug & 4) && threadIdx.x == 0) {
-        unsigned long long g_end;
-        unsigned smid;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_end));
-        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-        a.prof[blockIdx.y * 16 + 8] = g_start;
-        a.prof[blockIdx.y * 16 + 9] = g_end;
-        a.prof[blockIdx.y * 16 + 10] = smid;
-    }
 }
 
 // One warp per query: re-rank the slices' nominated centroids with the

@@ -48,7 +48,6 @@ int set_err(int code, const char* fmt, ...) {
     } while (0)
 
 std::atomic<long long> g_launches{0};
-unsigned long long* g_ws_prof = nullptr;  // debug profiling buffer (IVFPQ_WS_DEBUG bit 5)
 
 // After every kernel launch: count it (ivfpq_launch_count) and check it.
 #define KCHECK()                                              \
@@ -162,12 +161,6 @@ __global__ void interleave_codes_kernel(const uint8_t* __restrict__ src, const i
 }
 
 // qlist/qcount (optional): block b merges row b and writes it to row qlist[b], b < *qcount.
-__global__ void gtimer_kernel(unsigned long long* out) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    *out = t;
-}
-
 __global__ void merge_keys_kernel(const uint64_t* __restrict__ in, int W, int nq, int n_in, int n_out,
                                   uint64_t* __restrict__ out, const int* qlist = nullptr,
                                   const int* qcount = nullptr) {
@@ -425,68 +418,23 @@ int run_select_tc(ivfpq_index* idx, const float* d_q, int64_t nq, int64_t P, uin
     int* flist = fcount + 1;
     CK(cudaMemsetAsync(fcount, 0, sizeof(int), st));
     idx->tc_used = true;
-    static bool attr = false;
-    if (!attr) {
-        CKR(set_smem_attr((const void*)coarse_tc_kernel, coarse_tc_smem(TC_MAXD)));
-        attr = true;
-    }
-    CoarseTcArgs ta{d_q, idx->tc_img, cand, ncand, thr, (int)nq, (int)nc, (int)d, (int)tps, (int)nkc, 0, nullptr};
-    static const int tc_dbg = [] {
-        const char* e = getenv("IVFPQ_TC_DEBUG");
-        return e ? atoi(e) : 0;
-    }();
-    if (tc_dbg) {
-        static unsigned long long* prof = nullptr;
-        if (!prof) CK(cudaMalloc((void**)&prof, 4096 * 16 * 8));
-        ta.debug = tc_dbg;
-        ta.prof = prof;
-        g_ws_prof = prof;
-    }
-    cudaEvent_t ev[5];
-    const bool timing = (tc_dbg & 8) != 0;
-    if (timing) {
-        for (auto& e : ev) cudaEventCreate(&e);
-        cudaEventRecord(ev[0], st);
-        gtimer_kernel<<<1, 1, 0, st>>>(ta.prof + 4000 * 16);
-    }
+    // dynamic-smem attributes are per device context: set before every launch
+    CKR(set_smem_attr((const void*)coarse_tc_kernel, coarse_tc_smem(TC_MAXD)));
+    CoarseTcArgs ta{d_q, idx->tc_img, cand, ncand, thr, (int)nq, (int)nc, (int)d, (int)tps, (int)nkc};
     coarse_tc_kernel<<<dim3((unsigned)nsl, (unsigned)qblocks), TC_THREADS, coarse_tc_smem((int)d), st>>>(ta);
-    if (timing) {
-        gtimer_kernel<<<1, 1, 0, st>>>(ta.prof + 4000 * 16 + 1);
-        cudaEventRecord(ev[1], st);
-    }
     KCHECK();
     CoarseRerankArgs ra{d_q, idx->coarse, idx->l2g, cand, ncand, thr, d_keys, fcount, flist, idx->tc_cmax,
                         (int)nq, (int)nc, (int)d, (int)P, (int)nsl, select_mode() == 2};
     coarse_rerank_kernel<<<(unsigned)((nq + TC_RR_WARPS - 1) / TC_RR_WARPS), 32 * TC_RR_WARPS,
                            coarse_rerank_smem((int)nsl, (int)d), st>>>(ra);
     KCHECK();
-    if (timing) cudaEventRecord(ev[2], st);
     // exact re-do of flagged queries: grid-stride over the device-side list
     // (blocks past *fcount exit at once; no host round trip)
-    static bool rattr = false;
-    if (!rattr) {
-        CKR(set_smem_attr((const void*)coarse_redo_kernel, SMEM_LIMIT));
-        rattr = true;
-    }
+    CKR(set_smem_attr((const void*)coarse_redo_kernel, SMEM_LIMIT));
     coarse_redo_kernel<<<(unsigned)std::min<int64_t>(nq, 2 * idx->num_sms), TK_BLOCK,
                          coarse_redo_smem((int)P, (int)d), st>>>(d_q, idx->coarse, idx->l2g, (int)nc, (int)d, (int)P,
                                                                 fcount, flist, d_keys);
     KCHECK();
-    if (timing) cudaEventRecord(ev[3], st);
-    if (timing) {
-        cudaEventRecord(ev[4], st);
-        cudaEventSynchronize(ev[4]);
-        float ms[4];
-        for (int i = 0; i < 4; ++i) cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1]);
-        unsigned long long gt[2], cs[16];
-        cudaMemcpy(gt, ta.prof + 4000 * 16, 16, cudaMemcpyDeviceToHost);
-        cudaMemcpy(cs, ta.prof, 128, cudaMemcpyDeviceToHost);
-        fprintf(stderr, "marker->cta0 start %.1f us, cta0 end -> marker %.1f us\n", (cs[8] - gt[0]) / 1e3,
-                (gt[1] - cs[9]) / 1e3);
-        fprintf(stderr, "select_tc: tc %.1f us  rerank %.1f us  redo %.1f us  merge %.1f us\n", ms[0] * 1e3,
-                ms[1] * 1e3, ms[2] * 1e3, ms[3] * 1e3);
-        for (auto& e : ev) cudaEventDestroy(e);
-    }
     return IVFPQ_OK;
 }
 
@@ -547,7 +495,7 @@ int run_select(ivfpq_index* idx, const float* d_q, int64_t nq, int64_t P, uint64
 }
 
 struct WsPlan {
-    int G, NBUF, SD;
+    int G, NBUF;
     size_t smem;
     int gmem;
 };
@@ -577,7 +525,7 @@ bool ws_plan(const ivfpq_index* idx, int64_t P, int64_t K, int dt, WsPlan* plan)
     // rows per builder thread beyond the TMEM budget: codebook read from global
     const bool gmem = (idx->s_pad + R - 1) / R > jpt;
     const size_t lut_each = WsLayout((int)idx->d, (int)idx->s, (int)idx->sub_d, (int)idx->p, lut_bytes_of((int)dt), 1,
-                                     2, (int)K, 2, (int)idx->s_pad).lut_each;
+                                     2, (int)K, (int)idx->s_pad).lut_each;
     int G = (int)std::max<size_t>(1, std::min<size_t>(WS_MAX_G, lut_budget_bytes() / lut_each));
     G = (int)std::min<int64_t>(G, std::max<int64_t>(1, P));
     static const int env_nb = [] {
@@ -593,20 +541,14 @@ bool ws_plan(const ivfpq_index* idx, int64_t P, int64_t K, int dt, WsPlan* plan)
     // per-query kernel: cfg3 p8 with f16 LUTs of 120 KiB)
     for (int min_nb = 3; min_nb >= 1; --min_nb)
     for (G = G0; G >= (min_nb == 3 ? 2 : 1); --G)
-        for (int sd = 0; sd <= 0; ++sd)  // codes go L2 -> registers: no smem stages
-            for (int nb = env_nb ? env_nb : WS_MAX_NBUF; nb >= min_nb; --nb) {
-                const size_t sm = WsLayout((int)idx->d, (int)idx->s, (int)idx->sub_d, (int)idx->p, lut_bytes_of((int)dt),
-                                           G, nb, (int)K, sd, (int)idx->s_pad).total;
-                if (sm <= SMEM_LIMIT) {
-                    *plan = WsPlan{G, nb, sd, sm, gmem ? 1 : 0};
-                    static bool printed = false;
-                    if (!printed && getenv("IVFPQ_WS_PLAN_PRINT")) {
-                        fprintf(stderr, "scan_ws plan: G=%d NBUF=%d SD=%d smem=%zu\n", G, nb, sd, sm);
-                        printed = true;
-                    }
-                    return true;
-                }
+        for (int nb = env_nb ? env_nb : WS_MAX_NBUF; nb >= min_nb; --nb) {
+            const size_t sm = WsLayout((int)idx->d, (int)idx->s, (int)idx->sub_d, (int)idx->p, lut_bytes_of((int)dt), G,
+                                       nb, (int)K, (int)idx->s_pad).total;
+            if (sm <= SMEM_LIMIT) {
+                *plan = WsPlan{G, nb, sm, gmem ? 1 : 0};
+                return true;
             }
+        }
     return false;
 }
 
@@ -653,16 +595,13 @@ int run_scan(ivfpq_index* idx, const float* d_q, int64_t nq, const uint64_t* d_p
     a.s_pad = (int)idx->s_pad;
     a.K = (int)K;
     a.G = G;
-    a.debug_skip_gather = 0;
-    a.debug_skip_copy = 0;
-    a.debug_skip_ids = 0;
     a.out_keys = out_keys;
     a.out_ncand = out_ncand;
     a.out_ids = out_ids;
     a.out_dists = out_d;
     a.out_short = out_short;
     if (nq == 0) return IVFPQ_OK;
-    // v2 (persistent, warp-specialised, register-resident codebook) when the
+    // v2 (persistent, warp-specialised, codebook in tensor memory) when the
     // shape fits its register/smem budget; v1 otherwise.
     WsPlan plan;
     if (ws_plan(idx, P, K, dt, &plan)) {
@@ -670,31 +609,13 @@ int run_scan(ivfpq_index* idx, const float* d_q, int64_t nq, const uint64_t* d_p
         WsArgs w;
         w.a = a;
         w.NBUF = plan.NBUF;
-        w.SD = plan.SD;
         w.gmem = plan.gmem;
-        static const int dbg = [] {
-            const char* e = getenv("IVFPQ_WS_DEBUG");
-            return e ? atoi(e) : 0;
-        }();
-        w.debug = dbg;
-        w.a.debug_skip_gather = (dbg & 2) != 0;
-        w.a.debug_skip_copy = (dbg & 8) != 0;
-        w.a.debug_skip_ids = (dbg & 16) != 0;
-        w.prof = nullptr;
-        if (dbg & 32) {
-            static unsigned long long* prof = nullptr;
-            const size_t pb = (size_t)idx->num_sms * 32 * 8 * 8;
-            if (!prof) CK(cudaMalloc((void**)&prof, pb));
-            CK(cudaMemsetAsync(prof, 0, pb, st));
-            w.prof = prof;
-            g_ws_prof = prof;
-        }
         CKR(idx->work.ensure(16));
         w.work = idx->work.as<int>();
         CK(cudaMemsetAsync(w.work, 0, sizeof(int), st));
         // plan: job descriptors + residual rows per query
         const WsLayout lay((int)idx->d, (int)idx->s, (int)idx->sub_d, (int)idx->p, lut_bytes_of(dt), plan.G, plan.NBUF,
-                           (int)K, plan.SD, (int)idx->s_pad);
+                           (int)K, (int)idx->s_pad);
         const int d_pad = (int)lay.d_pad;
         const int JMAX = (int)std::max<int64_t>(1, (P + plan.G - 1) / plan.G);
         CKR(idx->plan_jobs.ensure((size_t)nq * JMAX * sizeof(WsJob)));
@@ -787,12 +708,6 @@ int ivfpq_debug_select_flagged(ivfpq_index* idx, int64_t* out) {
 }
 
 // Debug: copy the per-warp cycle counters of the last profiled launch.
-extern "C" int ivfpq_debug_ws_prof(void* host, int64_t bytes) {
-    if (!g_ws_prof) return set_err(IVFPQ_EINVAL, "no profiled launch");
-    CK(cudaDeviceSynchronize());
-    CK(cudaMemcpy(host, g_ws_prof, bytes, cudaMemcpyDeviceToHost));
-    return IVFPQ_OK;
-}
 
 int ivfpq_launch_count(int64_t* out) {
     if (!out) return set_err(IVFPQ_EINVAL, "null argument");

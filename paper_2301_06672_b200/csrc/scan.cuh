@@ -40,9 +40,6 @@ struct ScanArgs {
     const uint8_t* codes;     // interleaved, s_pad bytes per vector
     const float* centers;     // [s, 2^p, sub_d]
     int nq, d, P, s, sub_d, s_pad, K, G;
-    int debug_skip_gather;    // perf experiments only (IVFPQ_WS_DEBUG bit 1)
-    int debug_skip_copy;      // perf experiments only (IVFPQ_WS_DEBUG bit 3)
-    int debug_skip_ids;       // perf experiments only (IVFPQ_WS_DEBUG bit 4)
     // outputs: keys mode (multi-GPU) or final mode (single GPU)
     uint64_t* out_keys;       // [nq, K] or null
     int64_t* out_ncand;       // [nq] or null

@@ -4,28 +4,29 @@
 // scan_list :130-142, top_k :145-155) and as scan.cuh, restructured for B200:
 //
 //  * one CTA per SM (persistent), queries handed out by a global atomic;
-//  * the whole PQ codebook lives in TENSOR MEMORY (128 KiB of the SM's 256 KiB
-//    TMEM, tcgen05.alloc/st/ld): 16 BUILDER warps each read only their own
-//    lane's columns: builder thread t owns a quad of codes m = 4u..4u+3 and
-//    the subspaces j = jr, jr+R, ... (u = t % (N/4), jr = t / (N/4),
-//    R = 1024/N); one tcgen05.ld of a row's centers serves all G lists of a
-//    job.  Per (j, quad) one broadcast read of rq[j] feeds 4 table entries computed
-//    with packed f32x2 sub/mul/add (exact: every op is one IEEE rounding, in
-//    the reference order), then stored with one 4-, 8- or 16-byte STS:
+//  * the PQ codebook lives in TENSOR MEMORY (tcgen05.alloc/st/ld; up to 256 of
+//    the SM's 512 columns): each of the WS_BW = 8 BUILDER warps reads only its
+//    own lane's columns.  Builder thread t owns a quad of codes m = 4u..4u+3
+//    and the subspaces j = jr, jr+R, ... (u = t % (N/4), jr = t / (N/4),
+//    R = 4 * WS_NB / N); one tcgen05.ld of a row's centers serves all G lists
+//    of a job.  Per (j, quad) one broadcast read of rq[j] feeds 4 table
+//    entries computed with packed f32x2 sub/mul/add (every op one IEEE
+//    rounding, in the reference order), stored with one 4-, 8- or 16-byte STS:
 //      fp8: mul.rz.ftz.f32x2 by 2^-(127-bias) (exact scaling; values below
 //           min_normal become subnormal and flush to +0), then the code is
 //           min(bits >> (23-m), 255), done two-at-a-time with u16x2 min.
 //      f16: cvt.rn.satfinite.f16x2.f32 (= RNE of min(x, 65504)).
-//  * 15 SCANNER warps stream 32-vector code
-//    blocks (16-byte non-allocating loads, interleaved layout) and look the
-//    codes up in the slot's LUTs; R accumulates sequentially in j (fp32).
-//  * one PREP warp hands out queries, resolves probe keys 32 at a time and
-//    writes job descriptors + residuals into the slots ahead of the builders;
-//  * prep, builders and scanners exchange LUT slots (NBUF of them, each
-//    holding the LUTs of G probed lists of one query) through mbarriers:
-//    prep[] (1 arrival), full[] (256 builder arrivals) and empty[] (one
-//    arrival per scanner warp), so preparing job i+2, building job i+1 and
-//    scanning job i overlap and scanner warps never wait on each other.
+//  * WS_SW = 11 SCANNER warps take pairs of 32-vector code blocks (16-byte
+//    loads from L2 into registers, interleaved layout) and look the codes up
+//    in the slot's LUTs; R accumulates sequentially in j (fp32).
+//  * one PREP warp hands out queries and streams their planned jobs
+//    (ws_plan_kernel: descriptor + residual rows) into an 8-deep ring by TMA.
+//  * hand-offs: prep -> builders on mbarriers completed by the TMA (pfull);
+//    builders -> scanners on mbarriers (full, one arrival per builder warp);
+//    the two "slot free" hand-offs run on hardware NAMED barriers (bar.sync /
+//    bar.arrive): a role that waits for a free slot is descheduled instead of
+//    polling an mbarrier (measured: the polling loops of the builders and the
+//    prep warp issued ~20% of all instructions of the kernel).
 //  * top-k: each scanner warp filters against the query's shared threshold and
 //    appends survivors to a private smem buffer; a full buffer is rank-sorted
 //    and merged into the query's shared sorted list under a per-query lock.
@@ -58,13 +59,18 @@ constexpr int WS_MAX_NBUF = 6;
 #endif
 constexpr int WS_NQS = WS_NQS_CFG;           // per-query states (query top-k lists) in flight
 constexpr int WS_PD = 8;                     // prep ring depth (jobs prepared ahead)
-constexpr int WS_MAX_SD = 3;                 // code-block stages per scanner warp
 #ifndef WS_WBUF_CFG
 #define WS_WBUF_CFG 64
 #endif
 constexpr int WS_WBUF = WS_WBUF_CFG;         // per-warp candidate buffer
 constexpr int WS_MAX_K = 512;
-constexpr int WS_BAR_BUILD = 1;              // named barrier id for builders
+// Named barriers (16 per CTA; id 0 = __syncthreads):
+constexpr int WS_BAR_BUILD = 1;              // builders only (teardown)
+constexpr int WS_BAR_EMPTY0 = 2;             // + slot: LUT slot free   (builders sync, scanners arrive)
+constexpr int WS_BAR_PEMPTY0 = WS_BAR_EMPTY0 + WS_MAX_NBUF;  // + ring entry: prep entry consumed
+static_assert(WS_BAR_PEMPTY0 + WS_PD <= 16, "named barrier ids");
+constexpr int WS_BAR_EMPTY_N = WS_NB + WS_SW * 32;   // participants of a slot-free barrier
+constexpr int WS_BAR_PEMPTY_N = WS_NB + 32;          // participants of a ring-entry barrier
 
 
 struct WsJob;
@@ -76,12 +82,8 @@ struct WsArgs {
     const long long* plan_ncand; // [nq]
     int JMAX;
     int NBUF;
-    int SD;                // code-block stages per scanner warp (2..WS_MAX_SD)
     int gmem;              // 1: builders read the codebook from global memory (does not fit TMEM)
-    int debug;             // perf experiments only (wrong results): bit 0 = skip LUT math, bit 1 = skip
-                           // gathers + offers, bit 2 = scanners skip their blocks entirely
     int* work;             // global query counter (zeroed before launch)
-    unsigned long long* prof;  // debug bit 5: per-(CTA, warp) cycle counters [grid][32][8], else null
 };
 
 struct WsJob {
@@ -135,6 +137,19 @@ __device__ __forceinline__ u64 add2(u64 a, u64 b) {
         : "l"(a), "l"(b));
     return r;
 }
+// Packed add with flush-to-zero, for the LUT builders of the 8- and 16-bit
+// storage dtypes only.  ptxas does not fuse a mul.rn.f32x2 into an
+// add.rn.ftz.f32x2 (the FTZ modes differ; SASS-checked: FMUL2 + FADD2.FTZ),
+// and the result is identical after the storage encode: FTZ changes a sum
+// only when an operand or the result is below 2^-126, and then either the
+// other addend is >= 2^-102 (the flushed part is under half an ulp: same RNE
+// result) or the entry is < 2^-101, which f16 and e5m3/e4m4 store as +0
+// whether or not it was flushed.  The f32 LUT keeps the exact scalar adds.
+__device__ __forceinline__ u64 add2ftz(u64 a, u64 b) {
+    u64 r;
+    asm("add.rn.ftz.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
 // Packed add of two independent sums: (acc.x + x.x, acc.y + x.y), each one
 // fl(acc + x).  Only for addends that are not multiply results (LUT values),
 // so there is nothing for ptxas to contract.
@@ -168,15 +183,8 @@ __device__ __forceinline__ void mbar_arrive(u64* bar) {
                      (uint32_t)__cvta_generic_to_shared(bar))
                  : "memory");
 }
-// Critical-path wait (builders / scanners): try_wait with a suspend-time
-// hint -- the warp parks in NANOSLEEP.SYNCS and is woken by barrier traffic
-// (measured faster than a plain spin or a timed backoff here).
-// Builders waiting for a free LUT slot: 0 = suspend-hint wait, N > 0 =
-// exponential nanosleep backoff capped at N ns (does not spin on the issue
-// slots the scanners need).
-#ifndef WS_BUILDER_BACKOFF
-#define WS_BUILDER_BACKOFF 0
-#endif
+// Wait on an mbarrier phase: try_wait with a suspend-time hint (the warp parks
+// in NANOSLEEP.SYNCS and is woken by barrier traffic).
 #ifndef WS_WAIT_HINT_NS
 #define WS_WAIT_HINT_NS 1000000
 #endif
@@ -198,17 +206,6 @@ __device__ __forceinline__ bool mbar_try(u64* bar, uint32_t parity) {
         : "r"((uint32_t)__cvta_generic_to_shared(bar)), "r"(parity)
         : "memory");
     return ok != 0;
-}
-// Wait of a role that is normally ahead (prep warp, builders waiting for a
-// free LUT slot): exponential nanosleep backoff, so the waiting warp does
-// not take issue slots from the builders/scanners sharing its SMSP.
-template <int MAX_NS>
-__device__ __forceinline__ void mbar_wait_backoff(u64* bar, uint32_t parity) {
-    unsigned ns = 32;
-    while (!mbar_try(bar, parity)) {
-        __nanosleep(ns);
-        ns = ns * 2 > (unsigned)MAX_NS ? (unsigned)MAX_NS : ns * 2;
-    }
 }
 __device__ __forceinline__ void mbar_expect_tx(u64* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr_(bar)), "r"(bytes) : "memory");
@@ -235,6 +232,12 @@ __device__ __forceinline__ uint4 lds128(uint32_t a) {
     return r;
 }
 __device__ __forceinline__ void bar_builders() { asm volatile("bar.sync %0, %1;" ::"n"(WS_BAR_BUILD), "n"(WS_NB) : "memory"); }
+// Named-barrier hand-off: the consumer of a free slot waits with bar.sync (the
+// warp is descheduled, no polling), the releasing role signals with bar.arrive.
+__device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void nbar_arrive(int id, int n) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
 __device__ __forceinline__ float lds_f32(uint32_t a) {
     float v;
     asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
@@ -316,14 +319,15 @@ struct WsLayout {
     // Rows j >= s hold +0 entries (zero centers, zero residual), so the scan
     // reads whole 16-code chunks: the zero-code lookups past s add +0, which
     // leaves every sum bit-identical.
-    size_t bars, sbars, qfree, tmem, cnt, jobs, pjobs, prepq, qst, lists, wbuf, prq, stage, stage_bytes, lut, total, lut_each, d_pad;
-    __host__ __device__ WsLayout(int d, int s, int sub_d, int logn, int esize, int G, int NBUF, int K, int SD, int s_pad) {
+    size_t bars, qfree, tmem, cnt, jobs, pjobs, prepq, qst, lists, wbuf, prq, lut, total, lut_each, d_pad;
+    __host__ __device__ WsLayout(int d, int s, int sub_d, int logn, int esize, int G, int NBUF, int K, int s_pad) {
         const int N = 1 << logn, R = WS_R(N), jpt = (s_pad + R - 1) / R;
+        (void)d;
+        (void)s;
         lut_each = (((size_t)R * jpt * N * esize) + 255) & ~(size_t)255;  // 256-aligned (PRMT addressing)
         d_pad = (size_t)R * jpt * sub_d;
-        bars = 0;                                                         // pfull/pempty[PD], full/empty[MAX_NBUF]
-        sbars = (2 * WS_PD + 2 * WS_MAX_NBUF) * 8;                       // stage barriers [SW][MAX_SD]
-        qfree = sbars + WS_SW * WS_MAX_SD * 8;                            // query-state free barriers [NQS]
+        bars = 0;                                                         // pfull[PD], full[MAX_NBUF]
+        qfree = (WS_PD + WS_MAX_NBUF) * 8;                                // query-state free barriers [NQS]
         tmem = qfree + WS_NQS * 8;                                        // u32: TMEM base address
         cnt = tmem + 16;                                                  // int[MAX_NBUF]: next pair of each slot
         jobs = cnt + 32;                                                  // WsJob[MAX_NBUF] (LUT slots)
@@ -337,10 +341,7 @@ struct WsLayout {
         wbuf = lists + (size_t)WS_NQS * 2 * K * 8;                        // u64[SW][2][WBUF]
         prq = wbuf + (size_t)WS_SW * 2 * WS_WBUF * 8;                     // f32[PD][G][d_pad] (TMA-filled)
         prq = (prq + 127) & ~(size_t)127;
-        stage = prq + (size_t)WS_PD * G * d_pad * 4;                      // u8[SW][SD][32 * s_pad]
-        stage = (stage + 127) & ~(size_t)127;
-        stage_bytes = (size_t)32 * s_pad;
-        lut = stage + (size_t)WS_SW * SD * stage_bytes;                   // [NBUF][G][lut_each]
+        lut = prq + (size_t)WS_PD * G * d_pad * 4;                        // [NBUF][G][lut_each]
         lut = (lut + 255) & ~(size_t)255;
         total = lut + (size_t)NBUF * G * lut_each;
     }
@@ -502,8 +503,13 @@ struct WsBuild {
             const u64 d0 = sub2(cen[0][x], rr), d1 = sub2(cen[1][x], rr);
             const u64 q0 = mul2(d0, d0), q1 = mul2(d1, d1);
             // acc starts at +0: fl(0 + q) = q exactly (q >= +0)
-            acc0 = x == 0 ? q0 : add2(acc0, q0);
-            acc1 = x == 0 ? q1 : add2(acc1, q1);
+            if constexpr (DT == LUT_F32) {
+                acc0 = x == 0 ? q0 : add2(acc0, q0);
+                acc1 = x == 0 ? q1 : add2(acc1, q1);
+            } else {
+                acc0 = x == 0 ? q0 : add2ftz(acc0, q0);
+                acc1 = x == 0 ? q1 : add2ftz(acc1, q1);
+            }
         }
         store(dst, acc0, acc1);
     }
@@ -541,17 +547,10 @@ struct WsBuild {
 };
 
 // ------------------------------------------------------------- warp top-k
-// flush inlined: out of line it costs ~25% (call-site register spills, measured)
-#ifdef WS_FLUSH_NOINLINE
-#define WS_FLUSH_ATTR __device__ __noinline__
-#else
-#define WS_FLUSH_ATTR __device__ __forceinline__
-#endif
 struct WarpTopK {
     u64* buf;      // WS_WBUF
     u64* srt;      // WS_WBUF
     int n;         // warp-uniform count
-    unsigned long long* prof = nullptr;  // debug: [0] flushes, [2] locked flushes, [7] flush cycles
 
     __device__ __forceinline__ void offer(u64 key, bool pred) {
         const unsigned m = __ballot_sync(0xffffffffu, pred);
@@ -562,15 +561,8 @@ struct WarpTopK {
     // Merge the buffer into the query's shared list.  Candidates are first
     // re-filtered against the current threshold (it has usually tightened
     // since they were offered), so most flushes end without taking the lock.
-    WS_FLUSH_ATTR void flush(WsQuery* S, u64* lists, int K) {
-        const long long t0 = prof ? clock64() : 0;
-        flush_(S, lists, K);
-        if (prof && (threadIdx.x & 31) == 0) {
-            prof[0] += 1;
-            prof[7] += (unsigned long long)(clock64() - t0);
-        }
-    }
-    __device__ void flush_(WsQuery* S, u64* lists, int K) {
+    // Inlined: out of line it costs ~25% (call-site register spills, measured).
+    __device__ __forceinline__ void flush(WsQuery* S, u64* lists, int K) {
         const int lane = threadIdx.x & 31;
         __syncwarp();
         const u64 tau = *(volatile u64*)&S->tau;
@@ -585,6 +577,7 @@ struct WarpTopK {
         n = 0;
         if (m == 0) return;
         __syncwarp();
+        // rank sort; keys are unique (distinct vector ids), so ranks are a permutation
         for (int i = lane; i < m; i += 32) {
             const u64 x = srt[i];
             int r = 0;
@@ -593,11 +586,9 @@ struct WarpTopK {
         }
         __syncwarp();
         for (int i = lane; i < m; i += 32) srt[i] = buf[i];
-        const int n = m;
-        if (prof && lane == 0) prof[2] += 1;
         if (lane == 0) {
-            while (atomicCAS(&S->lock, 0, 1) != 0) {
-            }
+            // contended: back off so the spinning warp does not take issue slots
+            while (atomicCAS(&S->lock, 0, 1) != 0) __nanosleep(64);
             __threadfence_block();
         }
         __syncwarp();
@@ -606,10 +597,10 @@ struct WarpTopK {
         u64* O = lists + (size_t)(cur ^ 1) * K;
         for (int i = lane; i < K; i += 32) {
             const u64 a = A[i];
-            const int pos = i + lower_bound_u64(srt, n, a);
+            const int pos = i + lower_bound_u64(srt, m, a);
             if (pos < K) O[pos] = a;
         }
-        for (int i = lane; i < n; i += 32) {
+        for (int i = lane; i < m; i += 32) {
             const u64 b = srt[i];
             const int pos = i + lower_bound_u64(A, K, b);
             if (pos < K) O[pos] = b;
@@ -656,76 +647,53 @@ __device__ __forceinline__ float ws_gather(uint32_t word, uint32_t base) {
     }
 }
 
-template <int DT, int LOGN, int B>
-__device__ __forceinline__ float ws_acc1(float acc, uint4 w, uint32_t base, int nvalid, bool full) {
-    const uint32_t word = B < 4 ? w.x : B < 8 ? w.y : B < 12 ? w.z : w.w;
-    if (full || B < nvalid) acc = __fadd_rn(acc, ws_gather<DT, LOGN, B>(word, base));
-    return acc;
-}
-
-template <int DT, int LOGN>
-__device__ __forceinline__ float ws_acc16(float acc, uint4 w, uint32_t base, int nvalid, bool full) {
-    acc = ws_acc1<DT, LOGN, 0>(acc, w, base, nvalid, full);
-    acc = ws_acc1<DT, LOGN, 1>(acc, w, base, nvalid, full);
-    acc = ws_acc1<DT, LOGN, 2>(acc, w, base, nvalid, full);
-    acc = ws_acc1<DT, LOGN, 3>(acc, w, base, nvalid, full);
-    acc = ws_acc1<DT, LOGN, 4>(acc, w, base, nvalid, full);
-    acc = ws_acc1<DT, LOGN, 5>(acc, w, base, nvalid, full);
-    acc = ws_acc1<DT, LOGN, 6>(acc, w, base, nvalid, full);
-    acc = ws_acc1<DT, LOGN, 7>(acc, w, base, nvalid, full);
-    acc = ws_acc1<DT, LOGN, 8>(acc, w, base, nvalid, full);
-    acc = ws_acc1<DT, LOGN, 9>(acc, w, base, nvalid, full);
-    acc = ws_acc1<DT, LOGN, 10>(acc, w, base, nvalid, full);
-    acc = ws_acc1<DT, LOGN, 11>(acc, w, base, nvalid, full);
-    acc = ws_acc1<DT, LOGN, 12>(acc, w, base, nvalid, full);
-    acc = ws_acc1<DT, LOGN, 13>(acc, w, base, nvalid, full);
-    acc = ws_acc1<DT, LOGN, 14>(acc, w, base, nvalid, full);
-    acc = ws_acc1<DT, LOGN, 15>(acc, w, base, nvalid, full);
-    return acc;
-}
-
 // Two vectors per lane (consecutive blocks of the warp, possibly of two lists
 // with LUT bases ba / bb): the two sequential sums advance together in one
 // packed add per code -- 3.5 instructions per lookup instead of 4, and two
 // independent dependency chains.
 template <int DT, int LOGN, int B>
-__device__ __forceinline__ u64 ws_acc1x2(u64 acc, uint4 wa, uint4 wb, uint32_t ba, uint32_t bb, int nvalid,
-                                         bool full) {
+__device__ __forceinline__ u64 ws_acc1x2(u64 acc, uint4 wa, uint4 wb, uint32_t ba, uint32_t bb) {
     const uint32_t xa = B < 4 ? wa.x : B < 8 ? wa.y : B < 12 ? wa.z : wa.w;
     const uint32_t xb = B < 4 ? wb.x : B < 8 ? wb.y : B < 12 ? wb.z : wb.w;
-    if (full || B < nvalid) acc = addx2(acc, pk2(ws_gather<DT, LOGN, B>(xa, ba), ws_gather<DT, LOGN, B>(xb, bb)));
-    return acc;
+    return addx2(acc, pk2(ws_gather<DT, LOGN, B>(xa, ba), ws_gather<DT, LOGN, B>(xb, bb)));
 }
 
 template <int DT, int LOGN>
-__device__ __forceinline__ u64 ws_acc16x2(u64 acc, uint4 wa, uint4 wb, uint32_t ba, uint32_t bb, int nvalid,
-                                          bool full) {
-    acc = ws_acc1x2<DT, LOGN, 0>(acc, wa, wb, ba, bb, nvalid, full);
-    acc = ws_acc1x2<DT, LOGN, 1>(acc, wa, wb, ba, bb, nvalid, full);
-    acc = ws_acc1x2<DT, LOGN, 2>(acc, wa, wb, ba, bb, nvalid, full);
-    acc = ws_acc1x2<DT, LOGN, 3>(acc, wa, wb, ba, bb, nvalid, full);
-    acc = ws_acc1x2<DT, LOGN, 4>(acc, wa, wb, ba, bb, nvalid, full);
-    acc = ws_acc1x2<DT, LOGN, 5>(acc, wa, wb, ba, bb, nvalid, full);
-    acc = ws_acc1x2<DT, LOGN, 6>(acc, wa, wb, ba, bb, nvalid, full);
-    acc = ws_acc1x2<DT, LOGN, 7>(acc, wa, wb, ba, bb, nvalid, full);
-    acc = ws_acc1x2<DT, LOGN, 8>(acc, wa, wb, ba, bb, nvalid, full);
-    acc = ws_acc1x2<DT, LOGN, 9>(acc, wa, wb, ba, bb, nvalid, full);
-    acc = ws_acc1x2<DT, LOGN, 10>(acc, wa, wb, ba, bb, nvalid, full);
-    acc = ws_acc1x2<DT, LOGN, 11>(acc, wa, wb, ba, bb, nvalid, full);
-    acc = ws_acc1x2<DT, LOGN, 12>(acc, wa, wb, ba, bb, nvalid, full);
-    acc = ws_acc1x2<DT, LOGN, 13>(acc, wa, wb, ba, bb, nvalid, full);
-    acc = ws_acc1x2<DT, LOGN, 14>(acc, wa, wb, ba, bb, nvalid, full);
-    acc = ws_acc1x2<DT, LOGN, 15>(acc, wa, wb, ba, bb, nvalid, full);
+__device__ __forceinline__ u64 ws_acc16x2(u64 acc, uint4 wa, uint4 wb, uint32_t ba, uint32_t bb) {
+    acc = ws_acc1x2<DT, LOGN, 0>(acc, wa, wb, ba, bb);
+    acc = ws_acc1x2<DT, LOGN, 1>(acc, wa, wb, ba, bb);
+    acc = ws_acc1x2<DT, LOGN, 2>(acc, wa, wb, ba, bb);
+    acc = ws_acc1x2<DT, LOGN, 3>(acc, wa, wb, ba, bb);
+    acc = ws_acc1x2<DT, LOGN, 4>(acc, wa, wb, ba, bb);
+    acc = ws_acc1x2<DT, LOGN, 5>(acc, wa, wb, ba, bb);
+    acc = ws_acc1x2<DT, LOGN, 6>(acc, wa, wb, ba, bb);
+    acc = ws_acc1x2<DT, LOGN, 7>(acc, wa, wb, ba, bb);
+    acc = ws_acc1x2<DT, LOGN, 8>(acc, wa, wb, ba, bb);
+    acc = ws_acc1x2<DT, LOGN, 9>(acc, wa, wb, ba, bb);
+    acc = ws_acc1x2<DT, LOGN, 10>(acc, wa, wb, ba, bb);
+    acc = ws_acc1x2<DT, LOGN, 11>(acc, wa, wb, ba, bb);
+    acc = ws_acc1x2<DT, LOGN, 12>(acc, wa, wb, ba, bb);
+    acc = ws_acc1x2<DT, LOGN, 13>(acc, wa, wb, ba, bb);
+    acc = ws_acc1x2<DT, LOGN, 14>(acc, wa, wb, ba, bb);
+    acc = ws_acc1x2<DT, LOGN, 15>(acc, wa, wb, ba, bb);
     return acc;
 }
 
 // A pair of consecutive 32-vector blocks of one job (possibly of two lists
-// of the job), as handed to a scanner warp.
+// of the job), as handed to a scanner warp, with this lane's code source:
+// chunk c of the lane's vector in block b is at p[b] + c * st[b] (interleaved
+// layout).  Lanes past a block's vector count (and the whole
+// second block when the job has an odd block count) read a valid vector of
+// the pair instead -- their sums are never offered -- so the loads need no
+// branches.
 struct WsPair {
     uint32_t base0, base1;  // smem address of each block's LUT
     int nb0, nb1;           // vector count of each block (nb1 = 0: no second block)
     int vo0, vo1;           // first vector of each block (a device holds < 2^31 vectors)
     int qs;                 // query state of the job
+    const uint8_t* p0;
+    const uint8_t* p1;
+    uint32_t st0, st1;
 };
 
 // A job's list table held lane-parallel (lane g < ng describes list g), read
@@ -759,7 +727,7 @@ struct WsJobTab {
 // from the slot's counter (reset by the builders when they fill the slot), so
 // scanner warps finish a job within one pair of each other.
 __device__ __forceinline__ bool ws_grab(const WsJobTab& T, int* cnt, int slot, uint32_t slot_base, uint32_t lut_each,
-                                        int lane, WsPair& p) {
+                                        const uint8_t* codes, int s_pad, int lane, WsPair& p) {
     int k = 0;
     if (lane == 0) k = atomicAdd(cnt + slot, 1);
     k = __shfl_sync(0xffffffffu, k, 0);
@@ -776,21 +744,27 @@ __device__ __forceinline__ bool ws_grab(const WsJobTab& T, int* cnt, int slot, u
         p.nb1 = 0;
         p.vo1 = p.vo0;
     }
+    const int l0 = min(lane, p.nb0 - 1), l1 = min(lane, max(p.nb1 - 1, 0));
+    p.p0 = codes + (long long)p.vo0 * s_pad + l0 * 16;
+    p.p1 = codes + (long long)p.vo1 * s_pad + l1 * 16;
+    p.st0 = (uint32_t)p.nb0 * 16u;
+    p.st1 = (uint32_t)p.nb1 * 16u;
     return true;
 }
 
-// Chunk c (16 codes) of this lane's vector in a block: interleaved layout, so
-// a warp's 32 loads are 512 contiguous bytes.  Straight from L2 to registers.
-__device__ __forceinline__ uint4 ws_ld_chunk(const uint8_t* codes, int vo, int nb, int s_pad, int c, int lane) {
-    if (lane < nb) return ld_stream16(codes + (long long)vo * s_pad + c * nb * 16 + lane * 16);
-    return make_uint4(0u, 0u, 0u, 0u);
+__device__ __forceinline__ uint4 ws_ld(const uint8_t* p, u64 pol) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p), "l"(pol));
+    return r;
 }
 
 // End of this warp's part of the job in `slot`: at the query's last job, merge
 // the warp's candidates and let the last warp write the results and free the
-// query state; then release the LUT slot.
+// query state; then release the LUT slot (named barrier, see the header).
 __device__ __forceinline__ void ws_job_end(const ScanArgs& a, const WsJob* J, WsQuery* qst, u64* lists, int K,
-                                           WarpTopK& tk, u64* qfree, u64* empty_bar, int lane) {
+                                           WarpTopK& tk, u64* qfree, int slot, int lane) {
     if (J->last) {
         const int qs = J->qs;
         WsQuery* S = qst + qs;
@@ -831,34 +805,30 @@ __device__ __forceinline__ void ws_job_end(const ScanArgs& a, const WsJob* J, Ws
         }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(empty_bar);
+    nbar_arrive(WS_BAR_EMPTY0 + slot, WS_BAR_EMPTY_N);
 }
 
-// Scanner warp main loop.  Per pair: the 2 x nch chunk registers of the
-// current pair are consumed one chunk at a time and each freed register is
-// immediately refilled with the same chunk of the NEXT pair (or with chunk
-// c+4 of the current pair when nch > 4), so the L2 latency of a pair's codes
-// hides behind the scan of the previous pair.  The next pair comes from the
-// same job, else from the next job if its LUTs are already built.
-template <int DT, int LOGN>
-__device__ void ws_scanner(const ScanArgs& a, WsJob* jobs, int* cnt, u64* full, u64* empty, int NBUF, WsQuery* qst,
-                           u64* lists, int K, uint32_t lut_s0, uint32_t slot_bytes, uint32_t lut_each, WarpTopK& tk,
-                           u64* qfree, int lane, unsigned long long* prof) {
+// Scanner warp main loop.  Per pair: the 2 x min(nch, 4) chunk registers of
+// the current pair are consumed one chunk at a time and each freed register
+// is immediately refilled with chunk c+4 of the same pair, or (for the last
+// four chunks) with the same chunk of the NEXT pair, so the L2 latency of a
+// pair's codes hides behind the scan of the previous pair.  The next pair
+// comes from the same job, else from the next job if its LUTs are already
+// built.  NCH > 0: the chunk count s_pad/16 as a compile-time constant (the
+// BASELINE shapes; straight-line code), 0: read from the arguments.
+template <int DT, int LOGN, int NCH>
+__device__ void ws_scanner(const ScanArgs& a, WsJob* jobs, int* cnt, u64* full, int NBUF, WsQuery* qst, u64* lists,
+                           int K, uint32_t lut_s0, uint32_t slot_bytes, uint32_t lut_each, WarpTopK& tk, u64* qfree,
+                           int lane) {
     constexpr int N = 1 << LOGN;
     constexpr int E = (int)sizeof(typename LutTraits<DT>::T);
-    const int nch = a.s_pad >> 4, s_pad = a.s_pad;  // LUT rows >= s are +0: whole chunks are exact
-    // Code shape, measured on cfg2: the fp8 scans run 8% faster when the chunk
-    // loop keeps a (never taken at s % 16 == 0) partial-chunk branch, f16/f32
-    // 10% faster without it -- an instruction-scheduling effect of ptxas 12.9.
-    constexpr bool kSplit = DT == LUT_E5M3 || DT == LUT_E4M4;
-    const int nfull = kSplit ? a.s >> 4 : nch;
-    // debug profiling (IVFPQ_WS_DEBUG bit 5): cycles in blocking LUT waits,
-    // job ends, offers/flushes, next-pair grabs
-    long long t_wait = 0, t_end = 0, t_offer = 0, t_grab = 0, _t = 0;
-#define WS_S0() _t = prof ? clock64() : 0
-#define WS_S1(acc) acc += prof ? clock64() - _t : 0
+    constexpr int NS = NCH == 0 || NCH >= 4 ? 4 : NCH;  // chunk registers per block
+    const int nch = NCH > 0 ? NCH : a.s_pad >> 4;      // LUT rows >= s are +0: whole chunks are exact
+    const int s_pad = a.s_pad;
+    u64 pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
     const uint8_t* codes = a.codes;
-    uint4 A[4], B[4];
+    uint4 A[NS], B[NS];
     uint32_t idA = 0, idB = 0;
     int slot = 0, ph = 0;
     WsPair cur, nxt;
@@ -866,13 +836,13 @@ __device__ void ws_scanner(const ScanArgs& a, WsJob* jobs, int* cnt, u64* full, 
     mbar_wait(full, 0);
     if (jobs[0].qs < 0) return;
     ct.load(jobs, lane);
-    bool have = ws_grab(ct, cnt, 0, lut_s0, lut_each, lane, cur);
+    bool have = ws_grab(ct, cnt, 0, lut_s0, lut_each, codes, s_pad, lane, cur);
     auto load_first = [&](const WsPair& p) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < NS; ++u)
             if (u < nch) {
-                A[u] = ws_ld_chunk(codes, p.vo0, p.nb0, s_pad, u, lane);
-                B[u] = ws_ld_chunk(codes, p.vo1, p.nb1, s_pad, u, lane);
+                A[u] = ws_ld(p.p0 + u * p.st0, pol);
+                B[u] = ws_ld(p.p1 + u * p.st1, pol);
             }
         idA = lane < p.nb0 ? __ldg(a.ids + p.vo0 + lane) : 0u;
         idB = lane < p.nb1 ? __ldg(a.ids + p.vo1 + lane) : 0u;
@@ -880,25 +850,20 @@ __device__ void ws_scanner(const ScanArgs& a, WsJob* jobs, int* cnt, u64* full, 
     if (have) load_first(cur);
     while (true) {
         if (!have) {
-            WS_S0();
-            ws_job_end(a, jobs + slot, qst, lists, K, tk, qfree, empty + slot, lane);
-            WS_S1(t_end);
+            ws_job_end(a, jobs + slot, qst, lists, K, tk, qfree, slot, lane);
             if (++slot == NBUF) {
                 slot = 0;
                 ph ^= 1;
             }
-            WS_S0();
             mbar_wait(full + slot, ph);
-            WS_S1(t_wait);
             if (jobs[slot].qs < 0) break;
             ct.load(jobs + slot, lane);
-            have = ws_grab(ct, cnt, slot, lut_s0 + (uint32_t)slot * slot_bytes, lut_each, lane, cur);
+            have = ws_grab(ct, cnt, slot, lut_s0 + (uint32_t)slot * slot_bytes, lut_each, codes, s_pad, lane, cur);
             if (have) load_first(cur);
             continue;
         }
         // ---- the next pair: same job, else the next job if its LUTs are ready
-        WS_S0();
-        bool hn = ws_grab(ct, cnt, slot, lut_s0 + (uint32_t)slot * slot_bytes, lut_each, lane, nxt);
+        bool hn = ws_grab(ct, cnt, slot, lut_s0 + (uint32_t)slot * slot_bytes, lut_each, codes, s_pad, lane, nxt);
         bool cross = false;
         if (!hn) {
             const int ns = slot + 1 == NBUF ? 0 : slot + 1;
@@ -907,36 +872,34 @@ __device__ void ws_scanner(const ScanArgs& a, WsJob* jobs, int* cnt, u64* full, 
             // test as complete, so there is no cross-job prefetch)
             if (NBUF > 1 && mbar_test(full + ns, (uint32_t)nph) && jobs[ns].qs >= 0) {
                 nt.load(jobs + ns, lane);
-                hn = ws_grab(nt, cnt, ns, lut_s0 + (uint32_t)ns * slot_bytes, lut_each, lane, nxt);
+                hn = ws_grab(nt, cnt, ns, lut_s0 + (uint32_t)ns * slot_bytes, lut_each, codes, s_pad, lane, nxt);
                 cross = true;  // (an empty next job is left to the blocking path)
             }
         }
+        // without a next pair the refills re-read the current pair (L2 hits, discarded)
+        const uint8_t* n0 = hn ? nxt.p0 : cur.p0;
+        const uint8_t* n1 = hn ? nxt.p1 : cur.p1;
+        const uint32_t ns0 = hn ? nxt.st0 : cur.st0, ns1 = hn ? nxt.st1 : cur.st1;
         const uint32_t nidA = hn && lane < nxt.nb0 ? __ldg(a.ids + nxt.vo0 + lane) : 0u;
         const uint32_t nidB = hn && lane < nxt.nb1 ? __ldg(a.ids + nxt.vo1 + lane) : 0u;
-        WS_S1(t_grab);
         // ---- scan the current pair
         const uint32_t base0 = cur.base0, base1 = cur.base1;
         u64 acc = pk2(0.f, 0.f);
+#pragma unroll(NCH > 0 ? 1 : 1)
         for (int cg = 0; cg < nch; cg += 4) {
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int c = cg + u;
-                if (c < nch) {
+                if (u < NS && c < nch) {
                     const uint32_t o = (uint32_t)(c * 16 * N * E);
-                    if (!kSplit || c < nfull) acc = ws_acc16x2<DT, LOGN>(acc, A[u], B[u], base0 + o, base1 + o, 16, true);
-                    else acc = ws_acc16x2<DT, LOGN>(acc, A[u], B[u], base0 + o, base1 + o, a.s - 16 * c, false);
-                    if (c + 4 < nch) {
-                        A[u] = ws_ld_chunk(codes, cur.vo0, cur.nb0, s_pad, c + 4, lane);
-                        B[u] = ws_ld_chunk(codes, cur.vo1, cur.nb1, s_pad, c + 4, lane);
-                    } else if (hn) {
-                        A[u] = ws_ld_chunk(codes, nxt.vo0, nxt.nb0, s_pad, u, lane);
-                        B[u] = ws_ld_chunk(codes, nxt.vo1, nxt.nb1, s_pad, u, lane);
-                    }
+                    acc = ws_acc16x2<DT, LOGN>(acc, A[u], B[u], base0 + o, base1 + o);
+                    const bool same = c + 4 < nch;
+                    A[u] = ws_ld(same ? cur.p0 + (c + 4) * cur.st0 : n0 + u * ns0, pol);
+                    B[u] = ws_ld(same ? cur.p1 + (c + 4) * cur.st1 : n1 + u * ns1, pol);
                 }
             }
         }
         // ---- offers against the query's shared threshold
-        WS_S0();
         {
             float r0, r1;
             upk2(acc, r0, r1);
@@ -951,15 +914,12 @@ __device__ void ws_scanner(const ScanArgs& a, WsJob* jobs, int* cnt, u64* full, 
             tk.offer(k1, lane < cur.nb1 && k1 < tau);
             if (tk.n > WS_WBUF - 32) tk.flush(S, qlist, K);
         }
-        WS_S1(t_offer);
         if (!hn) {
             have = false;
             continue;
         }
         if (cross) {  // this warp's part of the current job is done
-            WS_S0();
-            ws_job_end(a, jobs + slot, qst, lists, K, tk, qfree, empty + slot, lane);
-            WS_S1(t_end);
+            ws_job_end(a, jobs + slot, qst, lists, K, tk, qfree, slot, lane);
             if (++slot == NBUF) {
                 slot = 0;
                 ph ^= 1;
@@ -970,22 +930,7 @@ __device__ void ws_scanner(const ScanArgs& a, WsJob* jobs, int* cnt, u64* full, 
         idA = nidA;
         idB = nidB;
     }
-    if (prof && lane == 0) {
-        atomicAdd(prof + 3, (unsigned long long)t_wait);
-        atomicAdd(prof + 4, (unsigned long long)t_end);
-        atomicAdd(prof + 5, (unsigned long long)t_offer);
-        atomicAdd(prof + 6, (unsigned long long)t_grab);
-    }
-#undef WS_S0
-#undef WS_S1
 }
-
-// debug profiling: accumulate clock64 deltas per warp (lane 0) into w.prof
-#define WS_T0() const long long _t0 = w.prof ? clock64() : 0
-#define WS_ACC(slot) \
-    do { \
-        if (w.prof && lane == 0) atomicAdd(w.prof + ((size_t)blockIdx.x * 32 + warp) * 8 + (slot), (unsigned long long)(clock64() - _t0)); \
-    } while (0)
 
 // ---------------------------------------------------------------- planning
 // One warp per query: resolve the probe keys (32 at a time) to owned,
@@ -1083,7 +1028,22 @@ __global__ void __launch_bounds__(256) ws_plan_kernel(const ScanArgs a, int G, i
         __syncwarp();
         pend = rest;
     }
-    if (nj == 0) emit(0, 0, true);  // no owned non-empty list: one empty last job
+    if (nj == 0) {
+        // no owned non-empty list: the result is the empty list, written here;
+        // the search kernel skips the query (no query state, no jobs)
+        for (int i = lane; i < a.K; i += 32) {
+            if (a.out_keys) {
+                a.out_keys[(size_t)q * a.K + i] = ~0ull;
+            } else {
+                a.out_ids[(size_t)q * a.K + i] = -1LL;
+                a.out_dists[(size_t)q * a.K + i] = __int_as_float(0x7f800000);
+            }
+        }
+        if (lane == 0) {
+            if (a.out_keys) a.out_ncand[q] = nc;
+            else a.out_short[q] = nc < a.K ? 1 : 0;
+        }
+    }
     if (lane == 0) {
         njobs[q] = nj;
         ncand[q] = nc;
@@ -1091,22 +1051,19 @@ __global__ void __launch_bounds__(256) ws_plan_kernel(const ScanArgs a, int G, i
 }
 #endif
 
-template <int DT, int LOGN, int SUB_D, bool GMEM>
+template <int DT, int LOGN, int SUB_D, bool GMEM, int NCH>
 __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) {
     using T = typename LutTraits<DT>::T;
     extern __shared__ __align__(1024) uint8_t ws_smem[];
     uint8_t* smem = ws_smem;
     const ScanArgs& a = w.a;
     const int G = a.G, NBUF = w.NBUF, K = a.K, NQS = WS_NQS;
-    const int SD = w.SD;
-    const WsLayout L(a.d, a.s, SUB_D, LOGN, (int)sizeof(T), G, NBUF, K, SD, a.s_pad);
+    const WsLayout L(a.d, a.s, SUB_D, LOGN, (int)sizeof(T), G, NBUF, K, a.s_pad);
     const size_t lut_each = L.lut_each;
     const int d_pad = (int)L.d_pad;
     const int jpt = (a.s_pad + WsBuild<DT, LOGN, SUB_D, GMEM>::R - 1) / WsBuild<DT, LOGN, SUB_D, GMEM>::R;  // rows per builder
-    u64* pfull = reinterpret_cast<u64*>(smem + L.bars);  // pfull[PD]: job + residuals prepared
-    u64* pempty = pfull + WS_PD;                          // pempty[PD]: prep entry consumed
-    u64* full = pempty + WS_PD;                           // full[NBUF]: LUTs ready
-    u64* empty = full + WS_MAX_NBUF;                      // empty[NBUF]: LUT slot free
+    u64* pfull = reinterpret_cast<u64*>(smem + L.bars);  // pfull[PD]: job + residuals prepared (TMA tx)
+    u64* full = pfull + WS_PD;                            // full[NBUF]: LUTs ready
     WsJob* jobs = reinterpret_cast<WsJob*>(smem + L.jobs);
     WsJob* pjobs = reinterpret_cast<WsJob*>(smem + L.pjobs);
     WsQuery* qst = reinterpret_cast<WsQuery*>(smem + L.qst);
@@ -1131,16 +1088,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.tmem);
     if (warp == 0) tmem_alloc<Builder::NCOL>(smem_addr(tmem_slot));
     if (threadIdx.x == 0) {
-        for (int b = 0; b < WS_PD; ++b) {
-            mbar_init(pfull + b, 1);
-            mbar_init(pempty + b, WS_BW);  // one arrival per builder warp
-        }
-        for (int b = 0; b < NBUF; ++b) {
-            mbar_init(full + b, WS_BW);
-            mbar_init(empty + b, WS_SW);
-        }
-        u64* sb = reinterpret_cast<u64*>(smem + L.sbars);
-        for (int b = 0; b < WS_SW * WS_MAX_SD; ++b) mbar_init(sb + b, 1);
+        for (int b = 0; b < WS_PD; ++b) mbar_init(pfull + b, 1);
+        for (int b = 0; b < NBUF; ++b) mbar_init(full + b, WS_BW);
         u64* qf = reinterpret_cast<u64*>(smem + L.qfree);
         for (int b = 0; b < WS_NQS; ++b) mbar_init(qf + b, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -1154,40 +1103,36 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
         // ============================ prep warp ============================
         // Hands out queries and streams their planned jobs (descriptor +
         // residual rows, from ws_plan_kernel) into the prep ring with TMA bulk
-        // copies, up to WS_PD jobs ahead of the builders.
+        // copies, up to WS_PD jobs ahead of the builders.  A ring entry is
+        // reused once the builders have released it (named barrier).
         int* pqs = reinterpret_cast<int*>(smem + L.prepq);
         const uint32_t pjob_bytes = (uint32_t)sizeof(WsJob), prq_bytes = (uint32_t)(G * d_pad * 4);
-        int job = 0, qseq = -1;
+        int job = 0, qseq = -1, ps = 0;
         while (true) {
             int q = 0;
             if (lane == 0) q = atomicAdd(w.work, 1);
             q = __shfl_sync(0xffffffffu, q, 0);
-            const int ps0 = job % WS_PD;
             if (q >= a.nq) {
-                if (job >= WS_PD) mbar_wait_backoff<256>(pempty + ps0, ((job / WS_PD) - 1) & 1);
+                if (job >= WS_PD) nbar_sync(WS_BAR_PEMPTY0 + ps, WS_BAR_PEMPTY_N);
                 if (lane == 0) {
-                    pqs[ps0] = -1;
-                    mbar_arrive(pfull + ps0);
+                    pqs[ps] = -1;
+                    mbar_arrive(pfull + ps);
                 }
                 break;
             }
+            const int nj = w.plan_njobs[q];
+            if (nj == 0) continue;  // no owned non-empty list: ws_plan_kernel wrote its result
             ++qseq;
             const int qs = qseq % NQS;
             WsQuery* S = qst + qs;
             // the state is reused only after the query that last held it was finalised
             if (qseq >= NQS) mbar_wait(reinterpret_cast<u64*>(smem + L.qfree) + qs, ((qseq / NQS) - 1) & 1);
-            const int nj = w.plan_njobs[q];
             if (lane == 0) {
                 S->q = q;
                 S->ncand = w.plan_ncand[q];
             }
             for (int j = 0; j < nj; ++j, ++job) {
-                const int ps = job % WS_PD;
-                {
-                    WS_T0();
-                    if (job >= WS_PD) mbar_wait_backoff<256>(pempty + ps, ((job / WS_PD) - 1) & 1);
-                    WS_ACC(0);
-                }
+                if (job >= WS_PD) nbar_sync(WS_BAR_PEMPTY0 + ps, WS_BAR_PEMPTY_N);
                 if (lane == 0) {
                     pqs[ps] = qs;
                     const size_t gj = (size_t)q * w.JMAX + j;
@@ -1196,6 +1141,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
                     bulk_g2s(smem_addr(pjobs + ps), w.plan_jobs + gj, pjob_bytes, pfull + ps);
                     bulk_g2s(smem_addr(prq + (size_t)ps * G * d_pad), w.plan_rq + gj * G * d_pad, prq_bytes, pfull + ps);
                 }
+                if (++ps == WS_PD) ps = 0;
             }
         }
     } else if (warp < WS_BW) {
@@ -1204,26 +1150,12 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
         Builder B;
         B.init(a.centers, a.s, t, tmem, w.gmem != 0);
         const uint32_t prq_s = smem_addr(prq), lut_s = smem_addr(lut_all);
-        int slot = 0, eph = 0;  // LUT slot of this job, parity of its previous release
+        int slot = 0, ps = 0, pph = 0;  // LUT slot, prep ring entry and its phase
         bool wrapped = false;
-        for (int job = 0;; ++job) {
-            const int ps = job % WS_PD;
-            {
-                WS_T0();
-                mbar_wait(pfull + ps, (job / WS_PD) & 1);
-                WS_ACC(0);
-            }
-            {
-                WS_T0();
-                if (wrapped) {
-#if WS_BUILDER_BACKOFF > 0
-                    mbar_wait_backoff<WS_BUILDER_BACKOFF>(empty + slot, eph);
-#else
-                    mbar_wait(empty + slot, eph);
-#endif
-                }
-                WS_ACC(1);
-            }
+        for (;;) {
+            mbar_wait(pfull + ps, pph);
+            // the slot's previous job has been scanned by every scanner warp
+            if (wrapped) nbar_sync(WS_BAR_EMPTY0 + slot, WS_BAR_EMPTY_N);
             const WsJob* PJ = pjobs + ps;
             const int pq_s = reinterpret_cast<const int*>(smem + L.prepq)[ps];
             if (t < 32) {  // the descriptor travels with the LUT slot (warp 0 copies it)
@@ -1241,21 +1173,17 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
                 if (lane == 0) mbar_arrive(full + slot);
                 break;
             }
-            {
-                WS_T0();
-                if (!(w.debug & 1))
-                    B.build(prq_s + (uint32_t)(ps * G * d_pad * 4), (uint32_t)(d_pad * 4),
-                            lut_s + (uint32_t)(slot * G * lut_each), (uint32_t)lut_each, PJ->ng, jpt);
-                WS_ACC(2);
-            }
-            __syncwarp();  // the warp's LUT stores / prep reads are ordered before its lane-0 arrivals
-            if (lane == 0) {
-                mbar_arrive(pempty + ps);
-                mbar_arrive(full + slot);
+            B.build(prq_s + (uint32_t)(ps * G * d_pad * 4), (uint32_t)(d_pad * 4),
+                    lut_s + (uint32_t)(slot * G * lut_each), (uint32_t)lut_each, PJ->ng, jpt);
+            __syncwarp();  // the warp's LUT stores / prep reads are ordered before its arrivals
+            if (lane == 0) mbar_arrive(full + slot);
+            nbar_arrive(WS_BAR_PEMPTY0 + ps, WS_BAR_PEMPTY_N);
+            if (++ps == WS_PD) {
+                ps = 0;
+                pph ^= 1;
             }
             if (++slot == NBUF) {
                 slot = 0;
-                if (wrapped) eph ^= 1;
                 wrapped = true;
             }
         }
@@ -1266,22 +1194,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
         const int sw = warp - WS_BW;
         u64* wb = reinterpret_cast<u64*>(smem + L.wbuf) + (size_t)sw * 2 * WS_WBUF;
         WarpTopK tk{wb, wb + WS_WBUF, 0};
-#ifdef WS_TK_PROF  // flush statistics (experiments only)
-        unsigned long long tkprof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        if (w.prof) tk.prof = tkprof;
-#endif
-        {
-            WS_T0();
-            ws_scanner<DT, LOGN>(a, jobs, reinterpret_cast<int*>(smem + L.cnt), full, empty, NBUF, qst, lists, K,
-                                 smem_addr(lut_all), (uint32_t)(G * lut_each), (uint32_t)lut_each, tk,
-                                 reinterpret_cast<u64*>(smem + L.qfree), lane,
-                                 w.prof ? w.prof + ((size_t)blockIdx.x * 32 + warp) * 8 : nullptr);
-            WS_ACC(1);
-        }
-#ifdef WS_TK_PROF
-        if (w.prof && lane == 0)
-            for (int i : {0, 2, 7}) atomicAdd(w.prof + ((size_t)blockIdx.x * 32 + warp) * 8 + i, tkprof[i]);
-#endif
+        ws_scanner<DT, LOGN, NCH>(a, jobs, reinterpret_cast<int*>(smem + L.cnt), full, NBUF, qst, lists, K,
+                                  smem_addr(lut_all), (uint32_t)(G * lut_each), (uint32_t)lut_each, tk,
+                                  reinterpret_cast<u64*>(smem + L.qfree), lane);
     }
 }
 

@@ -7,18 +7,35 @@
 
 namespace ivfpq {
 
+// The dynamic-smem attribute is per device context, so it is set before every
+// launch (cheap) instead of once per process.
+template <int DT, int LOGN, int SUB_D, bool GMEM, int NCH>
+cudaError_t ws_launch_k(const WsArgs& w, size_t smem, int grid, cudaStream_t st) {
+    cudaError_t e = cudaFuncSetAttribute(scan_ws_kernel<DT, LOGN, SUB_D, GMEM, NCH>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    scan_ws_kernel<DT, LOGN, SUB_D, GMEM, NCH><<<grid, WS_THREADS, smem, st>>>(w);
+    return cudaGetLastError();
+}
+
+// Chunk count (s_pad / 16) as a compile-time constant for the BASELINE shapes
+// (straight-line chunk loop), a runtime loop for every other shape:
+//   cfg1/cfg2 s=64, cfg4 s=48 (p=8, sub_d=2); cfg5 s=32 (sub_d=3);
+//   cfg3 s=240 (sub_d=4): p=8 with the codebook in global memory, p=5 in TMEM.
 template <int DT, int LOGN, int SUB_D, bool GMEM>
 cudaError_t ws_launch_g(const WsArgs& w, size_t smem, int grid, cudaStream_t st) {
-    static int ok = -1;
-    if (ok < 0) {
-        cudaError_t e = cudaFuncSetAttribute(scan_ws_kernel<DT, LOGN, SUB_D, GMEM>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        if (e != cudaSuccess) return e;
-        ok = 1;
+    const int nch = w.a.s_pad >> 4;
+    if constexpr (LOGN == 8 && SUB_D == 2 && !GMEM) {
+        if (nch == 4) return ws_launch_k<DT, LOGN, SUB_D, GMEM, 4>(w, smem, grid, st);
+        if (nch == 3) return ws_launch_k<DT, LOGN, SUB_D, GMEM, 3>(w, smem, grid, st);
     }
-    if (!ok) return cudaErrorNotSupported;
-    scan_ws_kernel<DT, LOGN, SUB_D, GMEM><<<grid, WS_THREADS, smem, st>>>(w);
-    return cudaGetLastError();
+    if constexpr (LOGN == 8 && SUB_D == 3 && !GMEM) {
+        if (nch == 2) return ws_launch_k<DT, LOGN, SUB_D, GMEM, 2>(w, smem, grid, st);
+    }
+    if constexpr (SUB_D == 4 && ((LOGN == 8 && GMEM) || (LOGN == 5 && !GMEM))) {
+        if (nch == 15) return ws_launch_k<DT, LOGN, SUB_D, GMEM, 15>(w, smem, grid, st);
+    }
+    return ws_launch_k<DT, LOGN, SUB_D, GMEM, 0>(w, smem, grid, st);
 }
 
 // GMEM: the builders read the codebook from global memory (it does not fit
