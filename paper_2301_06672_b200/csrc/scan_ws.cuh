@@ -436,14 +436,16 @@ struct WsBuild {
         }
     }
 
-    // The LUTs of ng lists: rq_s[g] (smem, d_pad floats) -> lut_s[g] (smem,
-    // R*jpt rows of N).  Centers of row i are read from TMEM once and reused
-    // for every list of the job.
-    __device__ __forceinline__ void build(uint32_t rq_s, uint32_t rq_stride, uint32_t lut_s, uint32_t lut_stride,
+    // The LUTs of ng lists: rq[g] (smem, d_pad floats) -> lut[g] (smem, R*jpt
+    // rows of N).  Centers of row i are read from TMEM once and reused for
+    // every list of the job.  The residual loads and table stores are plain
+    // C++ shared-memory accesses (not volatile asm), so ptxas can interleave
+    // the independent entry chains of the two rows and of consecutive lists.
+    __device__ __forceinline__ void build(const uint8_t* rq, uint32_t rq_stride, uint8_t* lut, uint32_t lut_stride,
                                           int ng, int jpt) const {
         constexpr int E = sizeof(T);
-        const uint32_t rqb = rq_s + (uint32_t)jr * SUB_D * 4;
-        const uint32_t lb = lut_s + ((uint32_t)jr * N + 4 * u) * E;
+        const uint8_t* rqb = rq + (size_t)jr * SUB_D * 4;
+        uint8_t* lb = lut + ((size_t)jr * N + 4 * u) * E;
         // two owned rows per iteration: 2 x ng independent entry chains in flight
         int i = 0;
 #pragma unroll 1
@@ -460,12 +462,28 @@ struct WsBuild {
                     cenA[h][x] = pk2(__uint_as_float(c0[(h * SUB_D + x) * 2]), __uint_as_float(c0[(h * SUB_D + x) * 2 + 1]));
                     cenB[h][x] = pk2(__uint_as_float(c1[(h * SUB_D + x) * 2]), __uint_as_float(c1[(h * SUB_D + x) * 2 + 1]));
                 }
-            const uint32_t raA = rqb + i * R * SUB_D * 4, laA = lb + i * R * N * E;
-            const uint32_t raB = raA + R * SUB_D * 4, laB = laA + R * N * E;
+            const uint8_t* raA = rqb + i * R * SUB_D * 4;
+            const uint8_t* raB = raA + R * SUB_D * 4;
+            uint8_t* laA = lb + (size_t)i * R * N * E;
+            uint8_t* laB = laA + (size_t)R * N * E;
+            // software-pipelined: the residuals of list g+1 are loaded before the
+            // stores of list g (the stores may alias them as far as ptxas knows);
+            // reading one list past the last is inside shared memory
+            float rA[SUB_D], rB[SUB_D];
+            load_rq(raA, rA);
+            load_rq(raB, rB);
 #pragma unroll 2
             for (int g = 0; g < ng; ++g) {
-                entry_quad(cenA, raA + g * rq_stride, laA + g * lut_stride);
-                entry_quad(cenB, raB + g * rq_stride, laB + g * lut_stride);
+                float nA[SUB_D], nB[SUB_D];
+                load_rq(raA + (g + 1) * rq_stride, nA);
+                load_rq(raB + (g + 1) * rq_stride, nB);
+                entry_quad(cenA, rA, laA + g * lut_stride);
+                entry_quad(cenB, rB, laB + g * lut_stride);
+#pragma unroll
+                for (int x = 0; x < SUB_D; ++x) {
+                    rA[x] = nA[x];
+                    rB[x] = nB[x];
+                }
             }
         }
         if (i < jpt) {
@@ -478,24 +496,41 @@ struct WsBuild {
 #pragma unroll
                 for (int x = 0; x < SUB_D; ++x)
                     cen[h][x] = pk2(__uint_as_float(c[(h * SUB_D + x) * 2]), __uint_as_float(c[(h * SUB_D + x) * 2 + 1]));
-            const uint32_t ra0 = rqb + i * R * SUB_D * 4, la0 = lb + i * R * N * E;
+            const uint8_t* ra0 = rqb + i * R * SUB_D * 4;
+            uint8_t* la0 = lb + (size_t)i * R * N * E;
+            float r0[SUB_D];
+            load_rq(ra0, r0);
 #pragma unroll 4
-            for (int g = 0; g < ng; ++g) entry_quad(cen, ra0 + g * rq_stride, la0 + g * lut_stride);
+            for (int g = 0; g < ng; ++g) {
+                float n0[SUB_D];
+                load_rq(ra0 + (g + 1) * rq_stride, n0);
+                entry_quad(cen, r0, la0 + g * lut_stride);
+#pragma unroll
+                for (int x = 0; x < SUB_D; ++x) r0[x] = n0[x];
+            }
         }
     }
 
     // Four LUT entries (codes 4u..4u+3 of one subspace row) for one list:
     // T = seq_x fl(acc + fl(fl(c - rq)^2)), then the storage encode.
-    __device__ __forceinline__ static void entry_quad(const u64 (&cen)[2][SUB_D], uint32_t ra, uint32_t dst) {
-        float r[SUB_D];
+    __device__ __forceinline__ static void load_rq(const uint8_t* ra, float (&r)[SUB_D]) {
         if constexpr (SUB_D == 2) {
-            lds_f32x2(ra, r[0], r[1]);
+            const float2 v = *reinterpret_cast<const float2*>(ra);
+            r[0] = v.x;
+            r[1] = v.y;
         } else if constexpr (SUB_D == 4) {
-            lds_f32x4(ra, r[0], r[1], r[2], r[3]);
+            const float4 v = *reinterpret_cast<const float4*>(ra);
+            r[0] = v.x;
+            r[1] = v.y;
+            r[2] = v.z;
+            r[3] = v.w;
         } else {
 #pragma unroll
-            for (int x = 0; x < SUB_D; ++x) r[x] = lds_f32(ra + 4 * x);
+            for (int x = 0; x < SUB_D; ++x) r[x] = reinterpret_cast<const float*>(ra)[x];
         }
+    }
+
+    __device__ __forceinline__ static void entry_quad(const u64 (&cen)[2][SUB_D], const float (&r)[SUB_D], uint8_t* dst) {
         u64 acc0 = 0, acc1 = 0;
 #pragma unroll
         for (int x = 0; x < SUB_D; ++x) {
@@ -514,17 +549,17 @@ struct WsBuild {
         store(dst, acc0, acc1);
     }
 
-    __device__ __forceinline__ static void store(uint32_t dst, u64 a01, u64 a23) {
+    __device__ __forceinline__ static void store(uint8_t* dst, u64 a01, u64 a23) {
         if constexpr (DT == LUT_F32) {
             float a0, a1, a2, a3;
             upk2(a01, a0, a1);
             upk2(a23, a2, a3);
-            sts_v4f(dst, a0, a1, a2, a3);
+            *reinterpret_cast<float4*>(dst) = make_float4(a0, a1, a2, a3);
         } else if constexpr (DT == LUT_F16) {
             float a0, a1, a2, a3;
             upk2(a01, a0, a1);
             upk2(a23, a2, a3);
-            sts_v2(dst, cvt_f16x2_sat(a0, a1), cvt_f16x2_sat(a2, a3));
+            *reinterpret_cast<uint2*>(dst) = make_uint2(cvt_f16x2_sat(a0, a1), cvt_f16x2_sat(a2, a3));
         } else {
             constexpr int M = LutTraits<DT>::m, BIAS = LutTraits<DT>::bias;
             // y = x * 2^-(127-bias), round-toward-zero + flush-to-zero: exact
@@ -541,7 +576,7 @@ struct WsBuild {
             uint32_t h23 = __byte_perm(__float_as_uint(f2), __float_as_uint(f3), 0x7632);
             h01 = min_u16x2(h01, lim | (lim << 16)) >> (7 - M);
             h23 = min_u16x2(h23, lim | (lim << 16)) >> (7 - M);
-            sts_b32(dst, __byte_perm(h01, h23, 0x6420));
+            *reinterpret_cast<uint32_t*>(dst) = __byte_perm(h01, h23, 0x6420);
         }
     }
 };
@@ -1149,7 +1184,6 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
         const int t = threadIdx.x;
         Builder B;
         B.init(a.centers, a.s, t, tmem, w.gmem != 0);
-        const uint32_t prq_s = smem_addr(prq), lut_s = smem_addr(lut_all);
         int slot = 0, ps = 0, pph = 0;  // LUT slot, prep ring entry and its phase
         bool wrapped = false;
         for (;;) {
@@ -1173,8 +1207,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
                 if (lane == 0) mbar_arrive(full + slot);
                 break;
             }
-            B.build(prq_s + (uint32_t)(ps * G * d_pad * 4), (uint32_t)(d_pad * 4),
-                    lut_s + (uint32_t)(slot * G * lut_each), (uint32_t)lut_each, PJ->ng, jpt);
+            B.build(reinterpret_cast<const uint8_t*>(prq) + (size_t)ps * G * d_pad * 4, (uint32_t)(d_pad * 4),
+                    lut_all + (size_t)slot * G * lut_each, (uint32_t)lut_each, PJ->ng, jpt);
             __syncwarp();  // the warp's LUT stores / prep reads are ordered before its arrivals
             if (lane == 0) mbar_arrive(full + slot);
             nbar_arrive(WS_BAR_PEMPTY0 + ps, WS_BAR_PEMPTY_N);
