@@ -52,6 +52,7 @@ constexpr int WS_PREP_WARP = WS_BW + WS_SW;   // warp 31: job preparation
 __host__ __device__ constexpr int WS_R(int N) { return WS_NB * 4 / N; }
 __host__ __device__ constexpr int WS_JPT(int sub_d) { return 64 / (sub_d * WS_BW / 4); }
 constexpr int WS_THREADS = (WS_BW + WS_SW + 1) * 32;
+
 constexpr int WS_MAX_G = 8;
 constexpr int WS_MAX_NBUF = 6;
 #ifndef WS_NQS_CFG
@@ -1136,6 +1137,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
 
     if (warp == WS_PREP_WARP) {
         // ============================ prep warp ============================
+
         // Hands out queries and streams their planned jobs (descriptor +
         // residual rows, from ws_plan_kernel) into the prep ring with TMA bulk
         // copies, up to WS_PD jobs ahead of the builders.  A ring entry is
@@ -1181,6 +1183,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
         }
     } else if (warp < WS_BW) {
         // =========================== builders ===========================
+
         const int t = threadIdx.x;
         Builder B;
         B.init(a.centers, a.s, t, tmem, w.gmem != 0);
@@ -1225,6 +1228,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
         if (warp == 0) tmem_dealloc<Builder::NCOL>(tmem);
     } else {
         // =========================== scanners ===========================
+
         const int sw = warp - WS_BW;
         u64* wb = reinterpret_cast<u64*>(smem + L.wbuf) + (size_t)sw * 2 * WS_WBUF;
         WarpTopK tk{wb, wb + WS_WBUF, 0};
