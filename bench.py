@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--sweep", action="store_true", help="also sweep nprobe 8..256 for every dtype")
     ap.add_argument("--quick", action="store_true", help="skip per-dtype table and roofline")
+    ap.add_argument("--builder", choices=["cpu", "gpu"], default=None,
+                    help="index builder (default: cpu at cfg1/cfg2, gpu above; the reference arm always uses cpu)")
     return ap.parse_args()
 
 
@@ -111,46 +113,51 @@ class Clocks:
 
 
 # ---------------------------------------------------------------- workload ----
-def load_workload(cfg_name, rank, world, need_gpu=True):
-    """Rank 0 generates data, builds the index (GPU, untimed) and exact GT;
-    other ranks load the arrays from a shared temp dir."""
+def load_workload(args, rank, world):
+    """Rank 0 generates the data and builds the index arrays (untimed; the
+    deterministic CPU builder at cfg1/cfg2, identical in both arms); other
+    ranks load them from a shared temp dir.  Returns (cfg, arrays, base,
+    queries)."""
     from harness import workload as W
-    import torch
-    import torch.distributed as dist
-
-    cfg = dict(W.CONFIGS[cfg_name])
-    shared = os.path.join(tempfile.gettempdir(), f"ivfpq_bench_{cfg_name}_{os.environ.get('MASTER_PORT', '0')}")
+    cfg = dict(W.CONFIGS[args.config])
+    cfg["name"] = args.config
+    cfg["builder"] = args.builder or W.DEFAULT_BUILDER.get(args.config, "gpu")
+    shared = os.path.join(tempfile.gettempdir(), f"ivfpq_bench_{args.config}_{os.environ.get('MASTER_PORT', '0')}")
+    base = None
     if rank == 0:
         t0 = time.time()
         base, queries = W.make_data(cfg)
         t1 = time.time()
-        idx = W.build_index_gpu(base, cfg["nlist"], cfg["s"], cfg["p"], seed=cfg["seed"])
-        t2 = time.time()
-        gt = W.ground_truth_gpu(base, queries, 10)
-        t3 = time.time()
-        log(f"[bench] data {t1 - t0:.1f}s index build {t2 - t1:.1f}s gt {t3 - t2:.1f}s")
-        del base
+        arr = W.build_arrays(cfg, base, cfg["builder"])
+        log(f"[bench] data {t1 - t0:.1f}s, index build ({cfg['builder']}) {time.time() - t1:.1f}s")
         if world > 1:
             os.makedirs(shared, exist_ok=True)
-            off, ids, codes = idx.csr()
-            np.savez(os.path.join(shared, "w.npz"), coarse=idx.coarse, centers=idx.cb.centers, off=off, ids=ids,
-                     codes=codes, queries=queries, gt=gt)
+            np.savez(os.path.join(shared, "w.npz"), queries=queries, **arr)
     if world > 1:
+        import torch.distributed as dist
         dist.barrier()
         if rank != 0:
-            from paper_2301_06672_b200.index import IvfPqIndex, PQCodebook
             z = np.load(os.path.join(shared, "w.npz"))
-            idx = IvfPqIndex.from_csr(z["coarse"], PQCodebook(centers=z["centers"], p=cfg["p"]), z["off"], z["ids"],
-                                      z["codes"])
-            queries, gt = z["queries"], z["gt"]
+            arr = {k: z[k] for k in ("coarse", "centers", "off", "ids", "codes")}
+            queries = z["queries"]
         dist.barrier()
-    return cfg, idx, queries, gt
+    cfg["digest"] = W.arrays_digest(arr, queries)
+    return cfg, arr, base, queries
 
 
 def workload_desc(cfg, nprobe, dtype):
     return (f"{cfg['name']}: {cfg['n'] // 1000}K x {cfg['d']} synthetic Gaussian mixture ({cfg['comps']} comps, "
             f"spread {cfg['spread']}), nlist {cfg['nlist']}, pq_dim {cfg['s']}, pq_bits {cfg['p']}, "
             f"nprobe {nprobe}, k {cfg['k']}, {cfg['nq']} queries, LUT {dtype}")
+
+
+def config_dict(cfg, P, dtype, world):
+    """The `config` object, identical in both arms (same_config)."""
+    return {"workload": workload_desc(cfg, P, dtype), "n": cfg["n"], "d": cfg["d"], "nlist": cfg["nlist"],
+            "pq_dim": cfg["s"], "pq_bits": cfg["p"], "nprobe": P, "k": cfg["k"], "queries": cfg["nq"], "lut": dtype,
+            "parallelism": "single GPU" if world == 1 else f"lists sharded over {world} GPUs",
+            "index": f"{cfg['builder']} builder (harness/workload.py), inputs sha1 {cfg['digest']}",
+            "l2": "flushed between timed steps (256 MiB write)"}
 
 
 # -------------------------------------------------------------- our arm -----
@@ -215,8 +222,15 @@ def run_ours(args, rank, world):
     from harness.workload import recall_at
     from paper_2301_06672_b200 import _lib
 
-    cfg, idx, queries, gt = load_workload(args.config, rank, world)
-    cfg["name"] = args.config
+    from harness import workload as W
+    cfg, arr, base, queries = load_workload(args, rank, world)
+    gt = None
+    if rank == 0:
+        t0 = time.time()
+        gt = W.ground_truth_gpu(base, queries, 10)   # K7, exact (datasets.py:179-201)
+        log(f"[bench] ground truth {time.time() - t0:.1f}s")
+    del base
+    idx = W.to_index(arr, cfg["p"])
     P = args.nprobe or cfg["nprobe"]
     k = cfg["k"]
     nq = queries.shape[0]
@@ -239,7 +253,7 @@ def run_ours(args, rank, world):
     launches = _lib.launch_count() - n0
     res = step()
     ids = res[0].cpu().numpy()
-    rec = recall_at(ids[:, :10], gt)
+    rec = recall_at(ids[:, :10], gt) if rank == 0 else 0.0
     ms = float(times.mean())
     value = nq / (ms / 1e3)
 
@@ -249,21 +263,17 @@ def run_ours(args, rank, world):
     line = {"metric": METRIC, "value": round(value, 1), "unit": "queries/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": f"f32 accumulate, {args.dtype} LUT", "data": "synthetic",
-            "config": {"workload": workload_desc(cfg, P, args.dtype), "n": cfg["n"], "d": cfg["d"],
-                       "nlist": cfg["nlist"], "pq_dim": cfg["s"], "pq_bits": cfg["p"], "nprobe": P, "k": k,
-                       "queries": nq, "lut": args.dtype,
-                       "parallelism": "single GPU" if world == 1 else f"lists sharded over {world} GPUs",
-                       "l2": "flushed between timed steps (256 MiB write)"},
+            "impl": "ours", "config": config_dict(cfg, P, args.dtype, world),
             f"recall@10": round(rec, 4), "e2e": e2e, "gpu_launches": int(launches), "clocks": clk}
 
     if not args.quick:
         line["per_dtype"] = per_dtype(srch, q_dev, gt, k, P, flush, torch, world, nq)
         if world == 1:
-            line["roofline"] = roofline(srch, idx, q_dev, k, P, args.dtype, flush, torch)
+            line["roofline"] = roofline(srch, idx, q_dev, k, P, args.dtype, flush, torch, args.config)
     if args.sweep:
         line["sweep"] = sweep(srch, q_dev, gt, k, flush, torch, world, nq, cfg["nlist"])
     if rank == 0 and world == 1 and not args.no_cpu:
-        line["cpu_baseline"] = cpu_baseline(idx, queries, gt, k, P, args.dtype, args.cpu_sample)
+        line["cpu_baseline"] = cpu_baseline(arr, queries, gt, k, P, args.dtype, args.cpu_sample)
     if rank == 0:
         print(json.dumps(line), flush=True)
 
@@ -308,6 +318,7 @@ def measure_e2e(srch, queries, k, P, prec, steps, flush, torch, world):
 
 
 def per_dtype(srch, q_dev, gt, k, P, flush, torch, world, nq, steps=3):
+    """QPS and recall@10 per LUT dtype at the same nprobe (recall on rank 0)."""
     from harness.workload import recall_at
     out = {}
     for prec in PRECS:
@@ -322,7 +333,7 @@ def per_dtype(srch, q_dev, gt, k, P, flush, torch, world, nq, steps=3):
         t = timed_steps(fn, steps, flush, torch, world)
         res = fn()
         out[prec] = {"qps": round(nq / (float(t.mean()) / 1e3), 1), "ms": round(float(t.mean()), 4),
-                     "recall@10": round(recall_at(res[0].cpu().numpy()[:, :10], gt), 4)}
+                     "recall@10": round(recall_at(res[0].cpu().numpy()[:, :10], gt), 4) if gt is not None else None}
     return out
 
 
@@ -335,7 +346,7 @@ def sweep(srch, q_dev, gt, k, flush, torch, world, nq, nlist):
     return out
 
 
-def roofline(srch, idx, q_dev, k, P, prec, flush, torch):
+def roofline(srch, idx, q_dev, k, P, prec, flush, torch, cfg_name):
     """Dominant kernel = the scan kernel (K2+K3+K4).  Algorithmic bytes per
     launch = sum over queries of the code bytes of the lists actually probed
     (SURVEY.md 8d): B = sum_q sum_{c in probes(q)} L_c * pq_dim."""
@@ -366,23 +377,29 @@ def roofline(srch, idx, q_dev, k, P, prec, flush, torch):
     except OSError:
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
-    traffic = None
+    # DRAM bytes (read + write) of ONE scan launch, measured by ncu on this
+    # config, nprobe and dtype (profiles/scan_traffic.json, with the capture
+    # it came from); null when no capture exists for this exact workload
+    traffic, traffic_src = None, None
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "scan_traffic.json")))
-        traffic = tr.get(prec)
-    except (OSError, ValueError):
+        ent = tr.get(f"{cfg_name}/nprobe{P}/{prec}")
+        if ent:
+            traffic, traffic_src = ent["bytes"], ent["source"]
+    except (OSError, ValueError, KeyError):
         pass
     return {"bound": "hbm", "kernel": f"scan_ws_kernel<{prec}> (K2 LUT build + K3 scan + K4 top-k)",
             "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
-            "traffic": traffic, "algorithmic_bytes_per_launch": int(B), "scan_ms": round(float(t_scan), 4),
+            "traffic": traffic, "traffic_source": traffic_src, "algorithmic_bytes_per_launch": int(B),
+            "scan_ms": round(float(t_scan), 4),
             "select_ms": round(float(t_sel), 4),
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"}
 
 
-def cpu_baseline(idx, queries, gt, k, P, prec, n_sample):
+def cpu_baseline(arr, queries, gt, k, P, prec, n_sample):
     from harness.cpu_baseline import CpuBaseline
     from harness.workload import recall_at
-    cb = CpuBaseline(idx)
+    cb = CpuBaseline(arr)
     n = n_sample or cb.size_for(queries, k, P, prec, seconds=20.0)  # pilot underestimates QPS ~2x
     qps, ids, wall = cb.run(queries[:n], k, P, prec)
     cb.close()
@@ -395,36 +412,42 @@ def cpu_baseline(idx, queries, gt, k, P, prec, n_sample):
 # --------------------------------------------------------- reference arm ----
 def run_reference(args, rank, world):
     """The reference's CPU algorithm (oracle port of search.py) on the box's
-    host cores, same workload / metric; rank 0 only."""
+    host cores, same workload / metric / config; rank 0 only.  Its inputs come
+    from the CPU builder (numpy + host BLAS): this process never loads the
+    product library."""
     if rank != 0:
         return
+    from harness import cpu_build
     from harness.cpu_baseline import CpuBaseline
     from harness.workload import recall_at
-    cfg, idx, queries, gt = load_workload(args.config, 0, 1)
-    cfg["name"] = args.config
+    args.builder = "cpu"
+    cfg, arr, base, queries = load_workload(args, 0, 1)
     P = args.nprobe or cfg["nprobe"]
     k = cfg["k"]
-    cb = CpuBaseline(idx)
+    cb = CpuBaseline(arr)
     # each step is a bounded sample sized so the whole run is ~90 s of host time
     n = args.cpu_sample or cb.size_for(queries, k, P, args.dtype, seconds=90.0 / (args.warmup + args.steps))
     nq = queries.shape[0]
-    total_q, total_t, rec = 0, 0.0, []
+    total_q, total_t, hits = 0, 0.0, []
     for i in range(args.warmup + args.steps):
         rows = (i * n + np.arange(n)) % nq
-        sample = queries[rows]
-        qps, ids, wall = cb.run(sample, k, P, args.dtype)
+        qps, ids, wall = cb.run(queries[rows], k, P, args.dtype)
         if i >= args.warmup:
-            total_q += sample.shape[0]
+            total_q += rows.size
             total_t += wall
-            rec.append(recall_at(ids[:, :10], gt[rows]))
+            hits.append((rows, ids[:, :10]))
     cb.close()
+    # recall on the timed rows: exact ground truth on the CPU (datasets.py:179-201)
+    rows = np.concatenate([h[0] for h in hits])
+    uniq, inv = np.unique(rows, return_inverse=True)
+    gt = cpu_build.ground_truth_cpu(base, queries[uniq], 10)[inv]
+    rec = recall_at(np.concatenate([h[1] for h in hits]), gt)
     value = total_q / total_t
     line = {"metric": METRIC, "value": round(value, 2), "unit": "queries/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(1e3 * total_t / args.steps, 2), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": f"f32 accumulate, {args.dtype} LUT",
-            "data": "synthetic", "impl": "reference",
-            "config": {"workload": workload_desc(cfg, P, args.dtype), "nprobe": P, "k": k, "lut": args.dtype},
-            "recall@10": round(float(np.mean(rec)), 4),
+            "data": "synthetic", "impl": "reference", "config": config_dict(cfg, P, args.dtype, world),
+            "recall@10": round(float(rec), 4),
             "cpu_baseline": {"value": round(value, 2), "unit": "queries/s", "cores": cb.workers, "kind": "port",
                              "sample": f"{n} queries per step, oracle/ivfpq_np (numpy restatement of the reference "
                                        f"search_batch, search.py:187-203) in {cb.workers} single-thread processes"},
@@ -432,12 +455,30 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def spawn_ranks(n):
+    """`bench.py --gpus N` outside torchrun: re-launch this command as N ranks
+    (one per GPU) under torch.distributed.run on 127.0.0.1."""
+    import socket
+    import subprocess
+    import torch
+    have = torch.cuda.device_count()
+    if have < n:
+        log(f"[bench] --gpus {n} needs {n} CUDA devices, found {have}")
+        sys.exit(1)
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.run(cmd).returncode)
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    if args.gpus != world and world == 1 and args.gpus > 1:
-        log("[bench] --gpus > 1 requires torchrun; running on 1 GPU")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        spawn_ranks(args.gpus)
     if args.impl == "reference":
         run_reference(args, rank, world)   # rank 0 only; no process group needed
         return

@@ -45,17 +45,17 @@ def _work(args):
 class CpuBaseline:
     """Holds a worker pool with the index loaded; `run` times one sample."""
 
-    def __init__(self, idx, workers: int | None = None):
+    def __init__(self, arrays: dict, workers: int | None = None):
+        """arrays: coarse, centers, off, ids, codes (CSR list order, codes (n, s))."""
         import multiprocessing as mp
         self.workers = workers or len(os.sched_getaffinity(0))
         self.tmp = tempfile.TemporaryDirectory(prefix="ivfpq_cpu_")
-        off, ids, codes = idx.csr()
-        for name, arr in (("coarse", idx.coarse), ("centers", idx.cb.centers), ("off", off), ("ids", ids),
-                          ("codes", codes)):
-            np.save(os.path.join(self.tmp.name, name + ".npy"), arr)
+        for name in ("coarse", "centers", "off", "ids", "codes"):
+            np.save(os.path.join(self.tmp.name, name + ".npy"), arrays[name])
         self.pool = mp.get_context("spawn").Pool(self.workers, initializer=_init, initargs=(self.tmp.name,))
         # warm every worker (imports + index load) outside any timed sample
-        self.pool.map(_work, [(np.zeros((1, idx.d), np.float32), 1, 1, "f32")] * self.workers)
+        d = arrays["coarse"].shape[1]
+        self.pool.map(_work, [(np.zeros((1, d), np.float32), 1, 1, "f32")] * self.workers)
 
     def run(self, queries: np.ndarray, k: int, nprobe: int, prec: str):
         """Returns (qps, ids, wall_s) for the sample, split evenly over workers."""

@@ -1,16 +1,21 @@
-"""Benchmark workload: synthetic data, an (untimed) GPU index builder and exact
-ground truth.  Harness code, not the product: it uses torch ops as plumbing to
-produce the inputs of the search path quickly at BASELINE.json sizes.
+"""Benchmark workload: BASELINE.json configs, synthetic data, index builders
+and exact ground truth.  Harness code, not the product.
 
-Index training is OUT OF SCOPE for the hot path:
-the index comes from the package's GPU builder (Lloyd iterations on a
-subsample; assignment and bit-exact PQ encoding by the product kernels).  The
-search kernels consume the resulting arrays exactly like a reference-built
-index.
+Index training is OUT OF SCOPE for the hot path;
+the search kernels consume the resulting arrays exactly like a
+reference-built index.  Two builders:
+
+* "cpu" (harness/cpu_build.py, numpy + host BLAS only): deterministic, used by
+  BOTH bench arms at cfg1/cfg2 so they search identical arrays, and the only
+  one the reference arm may use (it must not load the product library);
+* "gpu" (the package's `train.build_index`: Lloyd on a subsample, assignment
+  and bit-exact pq_encode by the product kernels): for cfg3..cfg5, whose CPU
+  build would take hours.
 """
 
 from __future__ import annotations
 
+import hashlib
 import os
 import sys
 
@@ -20,7 +25,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
-# BASELINE.json configs (SURVEY.md 8d generator proposals)
+from harness import cpu_build  # noqa: E402  (numpy only)
+
+# BASELINE.json configs; generator (comps, spread) per SURVEY.md 8(d), calibrated
+# per config (profiles/r02_calibration.txt)
 CONFIGS = {
     "cfg1": dict(n=100_000, d=128, nlist=1024, s=64, p=8, nq=1_000, nprobe=32, k=10, comps=16, spread=0.3, seed=1),
     "cfg2": dict(n=1_000_000, d=128, nlist=4096, s=64, p=8, nq=10_000, nprobe=32, k=10, comps=64, spread=0.3,
@@ -34,12 +42,40 @@ CONFIGS = {
     "cfg5": dict(n=100_000_000, d=96, nlist=65536, s=32, p=8, nq=10_000, nprobe=64, k=10, comps=1024, spread=0.3,
                  seed=5),
 }
+DEFAULT_BUILDER = {"cfg1": "cpu", "cfg2": "cpu"}
 
 
 def make_data(cfg):
-    from paper_2301_06672_b200.datasets import synth_gaussian_mixture_chunked
-    X = synth_gaussian_mixture_chunked(cfg["n"] + cfg["nq"], cfg["d"], cfg["comps"], cfg["spread"], cfg["seed"])
+    """(base, queries): one chunked mixture draw of n + nq rows, split."""
+    X = cpu_build.synth_chunked(cfg["n"] + cfg["nq"], cfg["d"], cfg["comps"], cfg["spread"], cfg["seed"])
     return X[:cfg["n"]], X[cfg["n"]:]
+
+
+def build_arrays(cfg, base, builder: str):
+    """-> dict(coarse, centers, off, ids, codes) in CSR list order."""
+    if builder == "cpu":
+        coarse, centers, off, ids, codes = cpu_build.build_index_cpu(base, cfg["nlist"], cfg["s"], cfg["p"],
+                                                                     seed=cfg["seed"])
+        return dict(coarse=coarse, centers=centers, off=off, ids=ids, codes=codes)
+    idx = build_index_gpu(base, cfg["nlist"], cfg["s"], cfg["p"], seed=cfg["seed"])
+    off, ids, codes = idx.csr()
+    return dict(coarse=idx.coarse, centers=idx.cb.centers, off=off, ids=ids, codes=codes)
+
+
+def arrays_digest(arr: dict, queries: np.ndarray) -> str:
+    """Short hash of the search inputs (both bench arms print it: same inputs)."""
+    h = hashlib.sha1()
+    for k in ("coarse", "centers", "off", "ids", "codes"):
+        h.update(np.ascontiguousarray(arr[k]).data)
+    h.update(np.ascontiguousarray(queries).data)
+    return h.hexdigest()[:16]
+
+
+def to_index(arr: dict, p: int):
+    """Product index object over the arrays (loads the product library)."""
+    from paper_2301_06672_b200.index import IvfPqIndex, PQCodebook
+    return IvfPqIndex.from_csr(arr["coarse"], PQCodebook(centers=arr["centers"], p=p), arr["off"], arr["ids"],
+                               arr["codes"])
 
 
 def build_index_gpu(base: np.ndarray, nlist: int, s: int, p: int, seed: int = 0, train_n: int = 262_144,

@@ -15,6 +15,11 @@
  *     first and raises ValueError with the reference's wording.
  *   - "host" entry points take host buffers and are synchronous; "_device"
  *     entry points take device pointers and are asynchronous on `stream`.
+ *   - an index handle is immutable after creation and may be shared by host
+ *     threads; calls on one handle are serialised on the host, and a call on
+ *     a different stream than the previous call first waits (stream-ordered,
+ *     via an event) for the previous call's device work, because the calls
+ *     share the handle's scratch buffers.
  *   - LUT dtypes: the reference's `LUT_PRECISIONS` (search.py:38).
  *   - Keys: uint64 (fp32 bits of the distance << 32 | id), ascending = the
  *     reference's lexicographic (distance, id) order (search.py:150); empty
@@ -125,6 +130,14 @@ int ivfpq_pq_encode_device(const float *d_x, int64_t n, int64_t d, const float *
                            const float *d_centers, int64_t s, int64_t p, uint8_t *d_codes, void *stream);
 int ivfpq_pq_encode(const float *x, int64_t n, int64_t d, const float *centers, int64_t s, int64_t p,
                     uint8_t *codes);
+/* compute_residuals (pq.py:54-63): out f32[n,d] = fl(x - c[assign]); assign
+ * i64[n] in [0, nc). */
+int ivfpq_compute_residuals(const float *x, int64_t n, int64_t d, const float *c, int64_t nc,
+                            const int64_t *assign, float *out);
+/* reconstruct (pq.py:113-127): out f32[n, s*sub_d] = the sub-centroids named
+ * by codes u8[n,s]. */
+int ivfpq_reconstruct(const uint8_t *codes, int64_t n, const float *centers, int64_t s, int64_t p, int64_t sub_d,
+                      float *out);
 /* assign_to_centroids (kmeans.py:49-69): nearest centroid under the expanded
  * squared L2 form clipped at 0, ties -> lower id; d2 may be NULL.  Parity is
  * decision-level (einsum's norm order at d >= 16 is not modelled). */
@@ -139,6 +152,9 @@ int ivfpq_assign(const float *x, int64_t n, int64_t d, const float *c, int64_t n
  * reference.  Reuses the K1 select path over the base rows.  A handle from
  * ivfpq_knn_create is searched with ivfpq_select_device (keys = d2 bits << 32
  * | row id) and freed with ivfpq_index_destroy. */
+/* squared_l2_to_all (datasets.py:166-176): out f32[n] = sequential fp32
+ * sum over t of fl(fl(base[i][t] - q[t])^2), bit-exact. */
+int ivfpq_squared_l2_to_all(const float *base, int64_t n, int64_t d, const float *q, float *out);
 int ivfpq_knn_create(int device, const float *base, int64_t n, int64_t d, ivfpq_index **out);
 int ivfpq_brute_force_knn(const float *base, int64_t n, int64_t d, const float *queries, int64_t nq, int64_t k,
                           int64_t *out_ids, float *out_dists);

@@ -54,6 +54,9 @@ SIGNATURES = {
     "ivfpq_pq_encode": [_P, _I64, _I64, _P, _I64, _I64, _P],
     "ivfpq_assign_device": [_P, _I64, _I64, _P, _I64, _P, _P, _P],
     "ivfpq_assign": [_P, _I64, _I64, _P, _I64, _P, _P],
+    "ivfpq_compute_residuals": [_P, _I64, _I64, _P, _I64, _P, _P],
+    "ivfpq_reconstruct": [_P, _I64, _P, _I64, _I64, _I64, _P],
+    "ivfpq_squared_l2_to_all": [_P, _I64, _I64, _P, _P],
     "ivfpq_knn_create": [_I32, _P, _I64, _I64, _P],
     "ivfpq_brute_force_knn": [_P, _I64, _I64, _P, _I64, _I64, _P, _P],
 }

@@ -225,4 +225,40 @@ __global__ void row_sqnorm_kernel(const float* __restrict__ C, int64_t nc, int d
     out[i] = acc;
 }
 
+// squared_l2_to_all (datasets.py:166-176): d2[i] = sequential fp32 sum over
+// t of fl(fl(base[i][t] - q[t])^2), one thread per base row (no FMA).
+__global__ void sq_l2_all_kernel(const float* __restrict__ base, int64_t n, int d, const float* __restrict__ q,
+                                 float* __restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float* b = base + i * d;
+    float acc = 0.0f;
+    for (int t = 0; t < d; ++t) {
+        const float df = __fsub_rn(b[t], q[t]);
+        acc = __fadd_rn(acc, __fmul_rn(df, df));
+    }
+    out[i] = acc;
+}
+
+// compute_residuals (pq.py:54-63): fl(x[i][t] - c[a[i]][t]).
+__global__ void residuals_kernel(const float* __restrict__ x, int64_t n, int d, const float* __restrict__ c,
+                                 const int64_t* __restrict__ a, float* __restrict__ out) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n * d) return;
+    const int64_t i = e / d;
+    const int t = (int)(e - i * d);
+    out[e] = __fsub_rn(x[e], c[a[i] * d + t]);
+}
+
+// reconstruct (pq.py:113-127): out[i][j*sub_d + t] = centers[j][codes[i][j]][t].
+__global__ void reconstruct_kernel(const uint8_t* __restrict__ codes, int64_t n, int s, int N, int sub_d,
+                                   const float* __restrict__ centers, float* __restrict__ out) {
+    const int d = s * sub_d;
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n * d) return;
+    const int64_t i = e / d;
+    const int r = (int)(e - i * d), j = r / sub_d, t = r - j * sub_d;
+    out[e] = centers[((int64_t)j * N + codes[i * s + j]) * sub_d + t];
+}
+
 }  // namespace ivfpq

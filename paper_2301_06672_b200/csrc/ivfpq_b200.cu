@@ -117,6 +117,10 @@ struct ivfpq_index {
     int64_t bytes = 0;
     cudaStream_t stream = nullptr;
     std::mutex mu;
+    // stream ordering of calls that share the scratch below (StreamOrder)
+    cudaEvent_t last_ev = nullptr;
+    cudaStream_t last_stream = nullptr;
+    bool last_used = false;
     // scratch
     DevBuf q, dist, pkeys, oids, odist, oshort, keys, ncand, work, plan_jobs, plan_rq, plan_nj, plan_nc, tc_sl, flags, glut;
     int num_sms = 0;
@@ -297,11 +301,7 @@ __global__ void topk_hook_kernel(const int64_t* ids, const float* dists, int n, 
 // ---- dispatch -------------------------------------------------------------------
 template <int DT, int LOGN>
 int launch_scan_t(const ScanArgs& a, size_t smem, void* glut, int grid, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        CK(cudaFuncSetAttribute(scan_kernel<DT, LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_LIMIT));
-        attr = true;
-    }
+    CK(cudaFuncSetAttribute(scan_kernel<DT, LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_LIMIT));  // per-device: set every launch
     scan_kernel<DT, LOGN><<<grid, TK_BLOCK, smem, st>>>(a, glut);
     KCHECK();
     return IVFPQ_OK;
@@ -349,6 +349,24 @@ int set_smem_attr(const void* fn, size_t bytes) {
 // the CUDA runtime (torch's default stream has handle 0).
 cudaStream_t pick_stream(ivfpq_index*, void* stream) { return reinterpret_cast<cudaStream_t>(stream); }
 
+// Every call on an index writes the index's scratch buffers (probe keys, job
+// plans, LUT scratch, staging).  Calls are serialised on the host by idx->mu;
+// on the device, a call issued on a different stream than the previous one
+// first waits for the previous call's work (event), so scratch is never
+// overwritten while an earlier call's kernels still read it.
+struct StreamOrder {
+    ivfpq_index* idx;
+    cudaStream_t st;
+    StreamOrder(ivfpq_index* i, cudaStream_t s) : idx(i), st(s) {
+        if (idx->last_used && idx->last_stream != st) cudaStreamWaitEvent(st, idx->last_ev, 0);
+    }
+    ~StreamOrder() {
+        cudaEventRecord(idx->last_ev, st);
+        idx->last_stream = st;
+        idx->last_used = true;
+    }
+};
+
 // 0 = auto (tensor-core K1 when the shape fits), 1 = SIMT only, 2 = tensor
 // core with every query re-done by the exact fallback (tests the fallback);
 // set by ivfpq_set_select_kernel or IVFPQ_SELECT_SIMT=1.
@@ -366,11 +384,7 @@ int select_mode() {
 
 int launch_coarse_topk(ivfpq_index* idx, const float* d_q, int64_t nq, int64_t P, int64_t nsl, int64_t slice,
                        uint64_t* out, const int* qlist, const int* qcount, cudaStream_t st, int64_t max_qblocks = 0) {
-    static bool attr = false;
-    if (!attr) {
-        CKR(set_smem_attr((const void*)coarse_topk_kernel, SMEM_LIMIT - 10 * 1024));
-        attr = true;
-    }
+    CKR(set_smem_attr((const void*)coarse_topk_kernel, SMEM_LIMIT - 10 * 1024));  // per-device: set every launch
     CoarseTopkArgs ca{d_q, idx->coarse, idx->l2g, out, (int)nq, (int)idx->nlist_local, (int)idx->d, (int)P, (int)slice};
     ca.qlist = qlist;
     ca.qcount = qcount;
@@ -383,11 +397,7 @@ int launch_coarse_topk(ivfpq_index* idx, const float* d_q, int64_t nq, int64_t P
 
 int launch_merge(const uint64_t* in, int64_t W, int64_t nq, int64_t P, uint64_t* out, const int* qlist,
                  const int* qcount, cudaStream_t st, int64_t max_blocks = 0) {
-    static bool mattr = false;
-    if (!mattr) {
-        CKR(set_smem_attr((const void*)merge_keys_kernel, SMEM_LIMIT));
-        mattr = true;
-    }
+    CKR(set_smem_attr((const void*)merge_keys_kernel, SMEM_LIMIT));  // per-device: set every launch
     const int64_t blocks = max_blocks > 0 ? std::min(nq, max_blocks) : nq;
     merge_keys_kernel<<<(unsigned)blocks, TK_BLOCK, topk_smem((int)P), st>>>(in, (int)W, (int)nq, (int)P, (int)P, out,
                                                                            qlist, qcount);
@@ -476,11 +486,7 @@ int run_select(ivfpq_index* idx, const float* d_q, int64_t nq, int64_t P, uint64
     int64_t rows = std::max<int64_t>(1, std::min<int64_t>(nq, (int64_t)(COARSE_CHUNK_BYTES / (nc * 4))));
     CKR(idx->dist.ensure((size_t)rows * nc * 4));
     const size_t sm = topk_smem((int)P);
-    static bool attr = false;
-    if (!attr) {
-        CKR(set_smem_attr((const void*)select_probes_kernel, SMEM_LIMIT));
-        attr = true;
-    }
+    CKR(set_smem_attr((const void*)select_probes_kernel, SMEM_LIMIT));  // per-device: set every launch
     for (int64_t r0 = 0; r0 < nq; r0 += rows) {
         const int64_t nr = std::min(rows, nq - r0);
         dim3 grid((unsigned)((nc + CL_BC - 1) / CL_BC), (unsigned)((nr + CL_BQ - 1) / CL_BQ));
@@ -803,6 +809,7 @@ int ivfpq_index_create(int device, const float* coarse, int64_t nlist, int64_t d
             return fail(set_err(IVFPQ_ECUDA, "%s failed: %s", #call, cudaGetErrorString(e_)));          \
     } while (0)
     CKI(cudaStreamCreateWithFlags(&idx->stream, cudaStreamNonBlocking));
+    CKI(cudaEventCreateWithFlags(&idx->last_ev, cudaEventDisableTiming));
     CKI(cudaDeviceGetAttribute(&idx->num_sms, cudaDevAttrMultiProcessorCount, device));
     auto up = [&](void** dst, const void* src, size_t bytes) -> cudaError_t {
         cudaError_t e = cudaMalloc(dst, std::max<size_t>(bytes, 16));
@@ -859,6 +866,7 @@ int ivfpq_index_destroy(ivfpq_index* idx) {
                       &idx->flags})
         b->release();
     if (idx->stream) cudaStreamDestroy(idx->stream);
+    if (idx->last_ev) cudaEventDestroy(idx->last_ev);
     delete idx;
     return IVFPQ_OK;
 }
@@ -875,6 +883,7 @@ int ivfpq_search(ivfpq_index* idx, const float* queries, int64_t nq, int64_t k, 
     std::lock_guard<std::mutex> lock(idx->mu);
     DeviceGuard guard(idx->device);
     cudaStream_t st = idx->stream;
+    StreamOrder order(idx, st);
     const int64_t nq1 = std::max<int64_t>(nq, 1);
     CKR(idx->q.ensure((size_t)nq1 * idx->d * 4));
     CKR(idx->oids.ensure((size_t)nq1 * k * 8));
@@ -902,7 +911,8 @@ int ivfpq_search_device(ivfpq_index* idx, const float* d_q, int64_t nq, int64_t 
     std::lock_guard<std::mutex> lock(idx->mu);
     DeviceGuard guard(idx->device);
     if (nq == 0) return IVFPQ_OK;
-    return search_device_impl(idx, d_q, nq, k, nprobe, dt, d_ids, d_d, d_short, pick_stream(idx, stream));
+    StreamOrder order(idx, pick_stream(idx, stream));
+    return search_device_impl(idx, d_q, nq, k, nprobe, dt, d_ids, d_d, d_short, order.st);
 }
 
 int ivfpq_select_device(ivfpq_index* idx, const float* d_q, int64_t nq, int64_t nprobe, uint64_t* d_keys,
@@ -913,7 +923,8 @@ int ivfpq_select_device(ivfpq_index* idx, const float* d_q, int64_t nq, int64_t 
     std::lock_guard<std::mutex> lock(idx->mu);
     DeviceGuard guard(idx->device);
     if (nq == 0) return IVFPQ_OK;
-    return run_select(idx, d_q, nq, nprobe, d_keys, pick_stream(idx, stream));
+    StreamOrder order(idx, pick_stream(idx, stream));
+    return run_select(idx, d_q, nq, nprobe, d_keys, order.st);
 }
 
 int ivfpq_merge_keys_device(const uint64_t* d_in, int64_t W, int64_t nq, int64_t n_in, int64_t n_out,
@@ -922,11 +933,7 @@ int ivfpq_merge_keys_device(const uint64_t* d_in, int64_t W, int64_t nq, int64_t
         return set_err(IVFPQ_EINVAL, "invalid merge shape W=%lld n_in=%lld n_out=%lld", (long long)W,
                        (long long)n_in, (long long)n_out);
     if (nq == 0) return IVFPQ_OK;
-    static bool attr = false;
-    if (!attr) {
-        CKR(set_smem_attr((const void*)merge_keys_kernel, SMEM_LIMIT));
-        attr = true;
-    }
+    CKR(set_smem_attr((const void*)merge_keys_kernel, SMEM_LIMIT));  // per-device: set every launch
     merge_keys_kernel<<<(unsigned)nq, TK_BLOCK, topk_smem((int)n_out), reinterpret_cast<cudaStream_t>(stream)>>>(
         d_in, (int)W, (int)nq, (int)n_in, (int)n_out, d_out);
     KCHECK();
@@ -938,8 +945,8 @@ int ivfpq_scan_device(ivfpq_index* idx, const float* d_q, int64_t nq, const uint
     CKR(validate_search(idx, nq, k, nprobe, dt));
     std::lock_guard<std::mutex> lock(idx->mu);
     DeviceGuard guard(idx->device);
-    return run_scan(idx, d_q, nq, d_pk, nprobe, k, dt, d_keys, d_ncand, nullptr, nullptr, nullptr,
-                    pick_stream(idx, stream));
+    StreamOrder order(idx, pick_stream(idx, stream));
+    return run_scan(idx, d_q, nq, d_pk, nprobe, k, dt, d_keys, d_ncand, nullptr, nullptr, nullptr, order.st);
 }
 
 int ivfpq_finalize_device(const uint64_t* d_keys, const int64_t* d_ncand, int64_t nq, int64_t k, int64_t* d_ids,
@@ -1098,7 +1105,20 @@ int ivfpq_scan_list(const uint8_t* codes, int64_t L, int64_t s, int64_t p, const
     CK(dent.alloc(ne * eb));
     CK(dout.alloc(L));
     CK(cudaMemcpy(dcodes.p, codes, L * s, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(dent.p, entries, ne * eb, cudaMemcpyHostToDevice));
+    if (dt == LUT_E5M3 || dt == LUT_E4M4) {
+        // The scan widens an fp8 entry with one shift (its value is scaled back
+        // once per vector), which is the exact decode for every code the
+        // encoder emits.  A caller-built table may also hold codes 1..2^m-1
+        // (zero exponent field), which the reference decodes to 0.0
+        // (minifloat.py:119-133): store those as 0 so the scan matches.
+        const int m = dt == LUT_E5M3 ? LutTraits<LUT_E5M3>::m : LutTraits<LUT_E4M4>::m;
+        std::vector<uint8_t> ent(static_cast<const uint8_t*>(entries), static_cast<const uint8_t*>(entries) + ne);
+        for (auto& e : ent)
+            if (e < (1u << m)) e = 0;
+        CK(cudaMemcpy(dent.p, ent.data(), ne, cudaMemcpyHostToDevice));
+    } else {
+        CK(cudaMemcpy(dent.p, entries, ne * eb, cudaMemcpyHostToDevice));
+    }
     CKR(DISPATCH_DT_LOGN(dt, (int)p, scan_list_dt, dcodes.p, L, (int)s, (const void*)dent.p, dout.p, ne * eb));
     CK(cudaMemcpy(out_r, dout.p, L * 4, cudaMemcpyDeviceToHost));
     return IVFPQ_OK;
@@ -1113,6 +1133,7 @@ int ivfpq_select_clusters(ivfpq_index* idx, const float* q, int64_t nq, int64_t 
     DeviceGuard guard(idx->device);
     if (nq == 0) return IVFPQ_OK;
     cudaStream_t st = idx->stream;
+    StreamOrder order(idx, st);
     CKR(idx->q.ensure((size_t)nq * idx->d * 4));
     CKR(idx->pkeys.ensure((size_t)nq * nprobe * 8));
     CKR(idx->oids.ensure((size_t)nq * nprobe * 8));
@@ -1212,6 +1233,61 @@ int ivfpq_pq_encode(const float* x, int64_t n, int64_t d, const float* centers, 
     return IVFPQ_OK;
 }
 
+int ivfpq_squared_l2_to_all(const float* base, int64_t n, int64_t d, const float* q, float* out) {
+    if (n < 0 || d < 1) return set_err(IVFPQ_EINVAL, "invalid shape n=%lld d=%lld", (long long)n, (long long)d);
+    if (n == 0) return IVFPQ_OK;
+    Tmp<float> db, dq, dout;
+    CK(db.alloc(n * d));
+    CK(dq.alloc(d));
+    CK(dout.alloc(n));
+    CK(cudaMemcpy(db.p, base, n * d * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dq.p, q, d * 4, cudaMemcpyHostToDevice));
+    sq_l2_all_kernel<<<blocks_for(n), 256>>>(db.p, n, (int)d, dq.p, dout.p);
+    KCHECK();
+    CK(cudaMemcpy(out, dout.p, n * 4, cudaMemcpyDeviceToHost));
+    return IVFPQ_OK;
+}
+
+int ivfpq_compute_residuals(const float* x, int64_t n, int64_t d, const float* c, int64_t nc, const int64_t* assign,
+                            float* out) {
+    if (n < 0 || d < 1 || nc < 1) return set_err(IVFPQ_EINVAL, "invalid shape");
+    for (int64_t i = 0; i < n; ++i)
+        if (assign[i] < 0 || assign[i] >= nc) return set_err(IVFPQ_EINVAL, "assignment index out of range");
+    if (n == 0) return IVFPQ_OK;
+    Tmp<float> dx, dc, dout;
+    Tmp<int64_t> da;
+    CK(dx.alloc(n * d));
+    CK(dc.alloc(nc * d));
+    CK(da.alloc(n));
+    CK(dout.alloc(n * d));
+    CK(cudaMemcpy(dx.p, x, n * d * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dc.p, c, nc * d * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(da.p, assign, n * 8, cudaMemcpyHostToDevice));
+    residuals_kernel<<<blocks_for(n * d), 256>>>(dx.p, n, (int)d, dc.p, da.p, dout.p);
+    KCHECK();
+    CK(cudaMemcpy(out, dout.p, n * d * 4, cudaMemcpyDeviceToHost));
+    return IVFPQ_OK;
+}
+
+int ivfpq_reconstruct(const uint8_t* codes, int64_t n, const float* centers, int64_t s, int64_t p, int64_t sub_d,
+                      float* out) {
+    if (n < 0 || s < 1 || p < 1 || p > 8 || sub_d < 1) return set_err(IVFPQ_EINVAL, "invalid shape");
+    for (int64_t i = 0; i < n * s; ++i)
+        if (codes[i] >= (1 << p)) return set_err(IVFPQ_EINVAL, "code byte out of range for p=%lld", (long long)p);
+    if (n == 0) return IVFPQ_OK;
+    Tmp<uint8_t> dk;
+    Tmp<float> dc, dout;
+    CK(dk.alloc(n * s));
+    CK(dc.alloc((s << p) * sub_d));
+    CK(dout.alloc(n * s * sub_d));
+    CK(cudaMemcpy(dk.p, codes, n * s, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dc.p, centers, (size_t)(s << p) * sub_d * 4, cudaMemcpyHostToDevice));
+    reconstruct_kernel<<<blocks_for(n * s * sub_d), 256>>>(dk.p, n, (int)s, 1 << (int)p, (int)sub_d, dc.p, dout.p);
+    KCHECK();
+    CK(cudaMemcpy(out, dout.p, n * s * sub_d * 4, cudaMemcpyDeviceToHost));
+    return IVFPQ_OK;
+}
+
 int ivfpq_assign_device(const float* d_x, int64_t n, int64_t d, const float* d_c, int64_t nc, int64_t* d_assign,
                         float* d_d2, void* stream) {
     if (n < 0 || d < 1) return set_err(IVFPQ_EINVAL, "invalid data shape");
@@ -1282,6 +1358,7 @@ int ivfpq_knn_create(int device, const float* base, int64_t n, int64_t d, ivfpq_
             return fail(set_err(IVFPQ_ECUDA, "%s failed: %s", #call, cudaGetErrorString(e_))); \
     } while (0)
     CKI(cudaStreamCreateWithFlags(&idx->stream, cudaStreamNonBlocking));
+    CKI(cudaEventCreateWithFlags(&idx->last_ev, cudaEventDisableTiming));
     CKI(cudaDeviceGetAttribute(&idx->num_sms, cudaDevAttrMultiProcessorCount, device));
     CKI(cudaMalloc((void**)&idx->coarse, (size_t)n * d * 4));
     CKI(cudaMemcpy(idx->coarse, base, (size_t)n * d * 4, cudaMemcpyHostToDevice));

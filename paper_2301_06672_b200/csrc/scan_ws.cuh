@@ -613,7 +613,7 @@ struct WarpTopK {
         n = 0;
         if (m == 0) return;
         __syncwarp();
-        // rank sort; keys are unique (distinct vector ids), so ranks are a permutation
+        // rank sort (keys are unique here: distinct vector ids)
         for (int i = lane; i < m; i += 32) {
             const u64 x = srt[i];
             int r = 0;

@@ -30,6 +30,19 @@ __device__ __forceinline__ int lower_bound_u64(const uint64_t* a, int n, uint64_
     }
     return lo;
 }
+__device__ __forceinline__ int upper_bound_u64(const uint64_t* a, int n, uint64_t x) {
+    int lo = 0, hi = n;  // count of a[i] <= x, a sorted ascending
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (a[mid] <= x) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+// Merge-path with equal keys: an element of the running list A goes before
+// the equal elements of the new sorted run (lower bound), a new element after
+// the equal elements of A (upper bound), so every output position is written
+// exactly once even when keys repeat (caller-supplied duplicate (id, dist)
+// pairs of the public top_k hook; reference np.lexsort keeps all copies).
 
 struct BlockTopK {
     uint64_t* slots[2];  // K keys each, ascending; slots[cur] is live
@@ -87,11 +100,11 @@ struct BlockTopK {
 
     __device__ void merge_n(const int n) {
         if (n == 0) return;  // uniform
-        // 1. rank-sort the (unique) candidates
+        // 1. rank-sort the candidates (stable: equal keys ranked by buffer index)
         for (int i = threadIdx.x; i < n; i += blockDim.x) {
             uint64_t x = buf[i];
             int r = 0;
-            for (int j = 0; j < n; ++j) r += buf[j] < x;
+            for (int j = 0; j < n; ++j) r += buf[j] < x || (buf[j] == x && j < i);
             sorted[r] = x;
         }
         __syncthreads();
@@ -105,7 +118,7 @@ struct BlockTopK {
         }
         for (int i = threadIdx.x; i < n; i += blockDim.x) {
             uint64_t b = sorted[i];
-            int pos = i + lower_bound_u64(A, K, b);
+            int pos = i + upper_bound_u64(A, K, b);
             if (pos < K) O[pos] = b;
         }
         __syncthreads();

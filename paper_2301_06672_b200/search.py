@@ -118,9 +118,18 @@ def scan_list(ids: np.ndarray, codes: np.ndarray, lut: Lut) -> tuple[np.ndarray,
     s, n_codes = entries.shape
     if codes.shape != (ids.shape[0], s):
         raise ValueError("codes shape must be (len(ids), s)")
-    codes = np.ascontiguousarray(codes, dtype=np.uint8)
-    if codes.size and int(codes.max()) >= n_codes:
+    # range check on the caller's array, before any narrowing (search.py:137-138)
+    if codes.size and codes.max() >= n_codes:
         raise ValueError("code byte out of range for the table")
+    if codes.size and not np.issubdtype(codes.dtype, np.integer):
+        raise IndexError("arrays used as indices must be of integer (or boolean) type")
+    if codes.size and codes.min() < 0:
+        # the reference indexes table[j, codes[:, j]]: numpy wraps negative
+        # indices in [-n_codes, -1] and raises IndexError below that
+        if codes.min() < -n_codes:
+            raise IndexError(f"index {int(codes.min())} is out of bounds for axis 1 with size {n_codes}")
+        codes = np.where(codes < 0, codes + n_codes, codes)
+    codes = np.ascontiguousarray(codes, dtype=np.uint8)
     p = int(n_codes).bit_length() - 1
     if 1 << p != n_codes:
         raise ValueError("table width must be a power of two")

@@ -135,7 +135,43 @@ def test_scan_list_known_answers(pkg):
     assert np.all(pkg.scan_list(np.arange(5), codes, lut)[1] == 0.0)
 
 
+def test_scan_list_code_range_and_zero_exponent_entries(pkg):
+    """Reference scan_list (search.py:130-142): the range check runs on the
+    caller's array (codes >= n_codes raise even when they would wrap in
+    uint8), negative codes index from the end as numpy does, and fp8 table
+    codes 1..2^m-1 decode to 0.0 (minifloat.py:119-133)."""
+    lut = pkg.Lut(entries=np.arange(16, dtype=np.float32).reshape(1, 16), precision="f32")
+    with pytest.raises(ValueError, match="out of range"):
+        pkg.scan_list(np.array([0]), np.array([[256 + 3]], dtype=np.int64), lut)
+    _, r = pkg.scan_list(np.array([0, 1]), np.array([[-1], [-16]], dtype=np.int64), lut)
+    assert r.tolist() == [15.0, 0.0]
+    with pytest.raises(IndexError):
+        pkg.scan_list(np.array([0]), np.array([[-17]], dtype=np.int64), lut)
+    from oracle import ivfpq_np as onp
+    rng = np.random.default_rng(11)
+    for prec, m in (("e5m3", 3), ("e4m4", 4)):
+        ent = rng.integers(0, 256, (8, 256)).astype(np.uint8)
+        ent[:, :16] = np.arange(16, dtype=np.uint8)          # includes the zero-exponent codes 1..2^m-1
+        codes = rng.integers(0, 256, (40, 8)).astype(np.uint8)
+        codes[:, 0] = np.arange(40) % 16
+        _, r = pkg.scan_list(np.arange(40), codes, pkg.Lut(entries=ent, precision=prec))
+        ro = onp.scan_list(codes, ent, prec)
+        assert np.array_equal(r, ro), prec
+
+
 # ------------------------------------------------------------------ K4 ----
+def test_top_k_duplicate_pairs(pkg):
+    """Repeated (id, dist) pairs are all kept, like np.lexsort."""
+    res = pkg.top_k(np.array([1, 1]), np.float32([0.5, 0.5]), k=2)
+    assert res.ids.tolist() == [1, 1] and res.distances.tolist() == [0.5, 0.5]
+    rng = np.random.default_rng(3)
+    ids = rng.integers(0, 20, 300)
+    d = rng.integers(0, 4, 300).astype(np.float32)
+    res = pkg.top_k(ids, d, 50)
+    o = np.lexsort((ids, d))[:50]
+    assert res.ids.tolist() == ids[o].tolist() and res.distances.tolist() == d[o].tolist()
+
+
 def test_top_k_known_answers(pkg):
     res = pkg.top_k(np.array([5, 2, 9]), np.float32([0.3, 0.1, 0.2]), k=10)
     assert res.ids.tolist() == [2, 9, 5] and res.short
@@ -314,6 +350,30 @@ def test_device_search_on_side_stream(pkg):
         pkg.search_device(dev, q, params, oi, od, osh)
         got = oi.cpu().numpy()
     assert np.array_equal(got, c["ids_f16_k10_p8"])
+
+
+def test_device_search_alternating_streams(pkg):
+    """Back-to-back calls on one index from two streams share its scratch;
+    the second call waits for the first (stream-ordered), so both results
+    are intact."""
+    import torch
+    c = load_case("sift_mini")
+    idx = index_from_case(c)
+    dev = pkg.device_index(idx)
+    q = torch.from_numpy(c["queries"]).cuda()
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = []
+    for rep in range(3):
+        for i, prec in enumerate(("e5m3", "f32")):
+            with torch.cuda.stream(streams[i]):
+                oi = torch.empty((q.shape[0], 10), dtype=torch.int64, device="cuda")
+                od = torch.empty((q.shape[0], 10), dtype=torch.float32, device="cuda")
+                osh = torch.empty(q.shape[0], dtype=torch.int32, device="cuda")
+                pkg.search_device(dev, q, pkg.SearchParams(k=10, nprobe=8, precision=prec), oi, od, osh)
+                outs.append((prec, oi))
+    torch.cuda.synchronize()
+    for prec, oi in outs:
+        assert np.array_equal(oi.cpu().numpy(), c[f"ids_{prec}_k10_p8"]), prec
 
 
 @pytest.mark.parametrize("nprobe,k", [(1, 10), (2, 5), (3, 100)])
