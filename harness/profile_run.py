@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--nprobe", type=int, default=None)
     ap.add_argument("--nq", type=int, default=0)
+    ap.add_argument("--builder", choices=["cpu", "gpu"], default=None)
     a = ap.parse_args()
     import torch
     from harness import workload as W
@@ -29,7 +30,9 @@ def main():
     base, queries = W.make_data(cfg)
     if a.nq:
         queries = queries[:a.nq]
-    idx = W.build_index_gpu(base, cfg["nlist"], cfg["s"], cfg["p"], seed=cfg["seed"])
+    # the same index bench.py measures (its default builder for the config)
+    idx = W.to_index(W.build_arrays(cfg, base, a.builder or W.DEFAULT_BUILDER.get(a.config, "gpu")), cfg["p"])
+    del base
     dev = DeviceIndex(idx, 0)
     q = torch.from_numpy(queries).cuda()
     k, P = cfg["k"], a.nprobe or cfg["nprobe"]
