@@ -1,0 +1,121 @@
+"""8-GPU readiness on ONE B200 (only one GPU is reachable here): the
+list-sharded protocol of parallel.py with W shards held as W device handles
+on the same GPU, each shard's work timed ALONE (CUDA events, L2 flushed):
+
+  T_shard(r) = local K1 (select over owned centroids) + probe merge
+             + local scan of the owned probed lists + top-k merge + finalize
+  T_1        = the single-handle search of the whole index (same kernels)
+  emulated speed-up = T_1 / (max_r T_shard(r) + T_allgather)
+
+T_allgather is not measurable on one GPU; it is estimated from the bytes the
+two all-gathers move (W x Q x nprobe x 8 and W x Q x k x 8) at the measured
+NVLink peer bandwidth (770 GB/s per direction, B200_PROFILING.md), plus 20 us
+of launch latency per collective.  The merged result of the W shards is
+checked bit-identical to the single-handle result.
+
+  python -m harness.shard_emulate --config cfg5 --world 8 --balance probe
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+NVLINK_GBS = 770.0
+COLL_LAT_S = 20e-6
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="cfg5")
+    ap.add_argument("--world", type=int, nargs="+", default=[2, 4, 8])
+    ap.add_argument("--dtype", default="e5m3")
+    ap.add_argument("--balance", choices=["bytes", "probe"], default="probe")
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--out", default="gpurun_out/shard_emulate.jsonl")
+    a = ap.parse_args()
+    import torch
+    from harness import workload as W
+    from paper_2301_06672_b200 import parallel
+    from paper_2301_06672_b200.index import DeviceIndex
+    cfg = W.CONFIGS[a.config]
+    t0 = time.time()
+    base, queries = W.make_data(cfg)
+    arr = W.build_arrays(cfg, base, W.DEFAULT_BUILDER.get(a.config, "gpu"))
+    # probe-frequency proxy from base rows (same distribution as the queries,
+    # disjoint from them): 20K rows
+    pseudo = base[np.random.default_rng(1).choice(base.shape[0], 20_000, replace=False)]
+    del base
+    idx = W.to_index(arr, cfg["p"])
+    lens = np.diff(arr["off"])
+    freq = parallel.probe_frequency(idx, pseudo, cfg["nprobe"]) if a.balance == "probe" else None
+    print(f"[shard] build {time.time() - t0:.1f}s", file=sys.stderr, flush=True)
+    k, P, nq = cfg["k"], cfg["nprobe"], queries.shape[0]
+    qd = torch.from_numpy(queries).cuda()
+    flush_buf = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+
+    def timed(fn, reps=a.reps):
+        out = fn()
+        ts = []
+        for _ in range(reps):
+            flush_buf.zero_()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            out = fn()
+            e1.record()
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return float(np.mean(ts)), out
+
+    full = parallel.CudaShardOps(DeviceIndex(idx, 0))
+
+    def single():
+        keys = full.select(qd, P)
+        sk, nc = full.scan(qd, keys, P, k, a.dtype)
+        return full.finalize(sk, nc, k)
+
+    t1, ref = timed(single)
+    ref_ids, ref_d = ref[0].cpu().numpy(), ref[1].cpu().numpy()
+    for world in a.world:
+        shards = parallel.shard_lists(lens, cfg["s"], world, freq)
+        ops = [parallel.CudaShardOps(DeviceIndex(idx, 0, owned=sh)) for sh in shards]
+        # stage 1: local K1 per shard, then the (replicated) probe merge
+        sel = [timed(lambda o=o: o.select(qd, P)) for o in ops]
+        stacked = torch.stack([s[1] for s in sel])
+        t_merge_p, probes = timed(lambda: ops[0].merge(stacked, P))
+        # stage 2: local scans, then the (replicated) top-k merge + finalize
+        scans = [timed(lambda o=o: o.scan(qd, probes, P, k, a.dtype)) for o in ops]
+        stacked_k = torch.stack([s[1][0] for s in scans])
+        ncand = scans[0][1][1]
+        t_merge_k, merged = timed(lambda: ops[0].merge(stacked_k, k))
+        t_fin, res = timed(lambda: ops[0].finalize(merged, ncand, k))
+        exact = bool(np.array_equal(res[0].cpu().numpy(), ref_ids) and np.array_equal(res[1].cpu().numpy(), ref_d))
+        per = [s[0] + t_merge_p + c[0] + t_merge_k + t_fin for s, c in zip(sel, scans)]
+        ag_bytes = [world * nq * P * 8, world * nq * k * 8]      # received per rank by each all-gather
+        t_ag = sum(b / (NVLINK_GBS * 1e9) + COLL_LAT_S for b in ag_bytes) * 1e3
+        owned_bytes = [int(lens[sh].sum()) * cfg["s"] for sh in shards]
+        row = {"config": a.config, "world": world, "dtype": a.dtype, "balance": a.balance,
+               "t1_ms": round(t1, 3), "t_shard_ms": [round(x, 3) for x in per],
+               "select_ms": [round(s[0], 3) for s in sel], "scan_ms": [round(c[0], 3) for c in scans],
+               "merge_probes_ms": round(t_merge_p, 3), "merge_topk_ms": round(t_merge_k + t_fin, 3),
+               "allgather_bytes_per_rank": ag_bytes, "allgather_est_ms": round(t_ag, 3),
+               "owned_code_bytes": owned_bytes,
+               "emulated_speedup": round(t1 / (max(per) + t_ag), 3), "bit_identical_to_1gpu": exact}
+        print(json.dumps(row), flush=True)
+        os.makedirs(os.path.dirname(a.out), exist_ok=True)
+        with open(a.out, "a") as f:
+            f.write(json.dumps(row) + "\n")
+        del ops
+
+
+if __name__ == "__main__":
+    main()

@@ -65,6 +65,7 @@ constexpr int WS_PD = 8;                     // prep ring depth (jobs prepared a
 #endif
 constexpr int WS_WBUF = WS_WBUF_CFG;         // per-warp candidate buffer
 constexpr int WS_MAX_K = 512;
+constexpr int WS_PRIV_K = 32;                // K up to which every scanner warp keeps private top-k lists
 // Named barriers (16 per CTA; id 0 = __syncthreads):
 constexpr int WS_BAR_BUILD = 1;              // builders only (teardown)
 constexpr int WS_BAR_EMPTY0 = 2;             // + slot: LUT slot free   (builders sync, scanners arrive)
@@ -337,9 +338,10 @@ struct WsLayout {
         prepq = pjobs + WS_PD * sizeof(WsJob);                            // int[PD]: query state of each prep entry
         qst = prepq + WS_PD * 4;                                          // WsQuery[NQS]
         qst = (qst + 15) & ~(size_t)15;
-        lists = qst + WS_NQS * sizeof(WsQuery);                           // u64[NQS][2][K]
-        lists = (lists + 15) & ~(size_t)15;
-        wbuf = lists + (size_t)WS_NQS * 2 * K * 8;                        // u64[SW][2][WBUF]
+        lists = qst + WS_NQS * sizeof(WsQuery);                           // top-k lists (WarpTopK):
+        lists = (lists + 15) & ~(size_t)15;                               //  u64[SW][NQS][K] (K <= WS_PRIV_K)
+        wbuf = lists + (size_t)(K <= WS_PRIV_K ? WS_SW * WS_NQS * K : WS_NQS * 2 * K) * 8;  // or u64[NQS][2][K]
+        //                                                                   u64[SW][2][WBUF]
         prq = wbuf + (size_t)WS_SW * 2 * WS_WBUF * 8;                     // f32[PD][G][d_pad] (TMA-filled)
         prq = (prq + 127) & ~(size_t)127;
         lut = prq + (size_t)WS_PD * G * d_pad * 4;                        // [NBUF][G][lut_each]
@@ -583,10 +585,21 @@ struct WsBuild {
 };
 
 // ------------------------------------------------------------- warp top-k
+// Top-k state per query.  Two layouts, chosen by K at launch:
+//  * K <= WS_PRIV_K ("private"): every scanner warp keeps its OWN sorted top-K
+//    per query state (lists[warp][qs][K]); a flush merges the warp's buffer
+//    into it and publishes its K-th key with a shared atomicMin into the
+//    query's threshold tau.  tau = min over warps of their K-th key is a valid
+//    filter: a key >= some warp's K-th key has K (unique) keys below it.  No
+//    lock; at the query's end the last warp merges the SW private lists.
+//  * larger K: one shared double-buffered list per query (lists[qs][2][K])
+//    merged under a per-query lock (smem budget: SW x NQS x K keys would not
+//    fit next to the LUT slots).
 struct WarpTopK {
     u64* buf;      // WS_WBUF
     u64* srt;      // WS_WBUF
     int n;         // warp-uniform count
+    u64* priv;     // private mode: this warp's lists[sw][0..NQS)[K], else null
 
     __device__ __forceinline__ void offer(u64 key, bool pred) {
         const unsigned m = __ballot_sync(0xffffffffu, pred);
@@ -594,11 +607,11 @@ struct WarpTopK {
         n += __popc(m);
     }
 
-    // Merge the buffer into the query's shared list.  Candidates are first
-    // re-filtered against the current threshold (it has usually tightened
-    // since they were offered), so most flushes end without taking the lock.
+    // Merge the buffer into the query's list (private or shared).  Candidates
+    // are first re-filtered against the current threshold (it has usually
+    // tightened since they were offered), so most flushes end early.
     // Inlined: out of line it costs ~25% (call-site register spills, measured).
-    __device__ __forceinline__ void flush(WsQuery* S, u64* lists, int K) {
+    __device__ __forceinline__ void flush(WsQuery* S, u64* lists, int qs, int K) {
         const int lane = threadIdx.x & 31;
         __syncwarp();
         const u64 tau = *(volatile u64*)&S->tau;
@@ -621,6 +634,26 @@ struct WarpTopK {
             buf[r] = x;
         }
         __syncwarp();
+        if (priv) {
+            // merge-path of the warp's list P (K) and the sorted run buf (m) into srt
+            u64* P = priv + (size_t)qs * K;
+            for (int i = lane; i < K; i += 32) {
+                const u64 a = P[i];
+                const int pos = i + lower_bound_u64(buf, m, a);
+                if (pos < K) srt[pos] = a;
+            }
+            for (int i = lane; i < m; i += 32) {
+                const u64 b = buf[i];
+                const int pos = i + lower_bound_u64(P, K, b);
+                if (pos < K) srt[pos] = b;
+            }
+            __syncwarp();
+            for (int i = lane; i < K; i += 32) P[i] = srt[i];
+            __syncwarp();
+            if (lane == 0 && srt[K - 1] != ~0ull) atomicMin(reinterpret_cast<unsigned long long*>(&S->tau), srt[K - 1]);
+            __syncwarp();
+            return;
+        }
         for (int i = lane; i < m; i += 32) srt[i] = buf[i];
         if (lane == 0) {
             // contended: back off so the spinning warp does not take issue slots
@@ -628,9 +661,10 @@ struct WarpTopK {
             __threadfence_block();
         }
         __syncwarp();
+        u64* qlist = lists + (size_t)qs * 2 * K;
         const int cur = *(volatile int*)&S->cur;
-        const u64* A = lists + (size_t)cur * K;
-        u64* O = lists + (size_t)(cur ^ 1) * K;
+        const u64* A = qlist + (size_t)cur * K;
+        u64* O = qlist + (size_t)(cur ^ 1) * K;
         for (int i = lane; i < K; i += 32) {
             const u64 a = A[i];
             const int pos = i + lower_bound_u64(srt, m, a);
@@ -804,15 +838,43 @@ __device__ __forceinline__ void ws_job_end(const ScanArgs& a, const WsJob* J, Ws
     if (J->last) {
         const int qs = J->qs;
         WsQuery* S = qst + qs;
-        u64* qlist = lists + (size_t)qs * 2 * K;
-        if (tk.n > 0) tk.flush(S, qlist, K);
+        if (tk.n > 0) tk.flush(S, lists, qs, K);
+        __syncwarp();
         int d = 0;
-        if (lane == 0) d = atomicAdd(&S->done, 1);
+        if (lane == 0) {
+            __threadfence_block();  // this warp's list before its arrival
+            d = atomicAdd(&S->done, 1);
+        }
         d = __shfl_sync(0xffffffffu, d, 0);
         if (d == WS_SW - 1) {
             __threadfence_block();
-            const int cur = *(volatile int*)&S->cur;
-            const u64* r = qlist + (size_t)cur * K;
+            const u64* r;
+            if (tk.priv) {
+                // merge the SW private lists of this query: running result in buf
+                const size_t wstride = (size_t)WS_NQS * K;
+                const u64* L0 = lists + (size_t)qs * K;
+                for (int i = lane; i < K; i += 32) tk.buf[i] = L0[i];
+                for (int w = 1; w < WS_SW; ++w) {
+                    const u64* Lw = L0 + w * wstride;
+                    __syncwarp();
+                    for (int i = lane; i < K; i += 32) {
+                        const u64 x = tk.buf[i];
+                        const int pos = i + lower_bound_u64(Lw, K, x);
+                        if (pos < K) tk.srt[pos] = x;
+                    }
+                    for (int i = lane; i < K; i += 32) {
+                        const u64 y = Lw[i];
+                        const int pos = i + upper_bound_u64(tk.buf, K, y);
+                        if (pos < K) tk.srt[pos] = y;
+                    }
+                    __syncwarp();
+                    for (int i = lane; i < K; i += 32) tk.buf[i] = tk.srt[i];
+                }
+                __syncwarp();
+                r = tk.buf;
+            } else {
+                r = lists + (size_t)qs * 2 * K + (size_t)(*(volatile int*)&S->cur) * K;
+            }
             const int q = S->q;
             const long long nc = S->ncand;
             for (int i = lane; i < K; i += 32) {
@@ -830,12 +892,19 @@ __device__ __forceinline__ void ws_job_end(const ScanArgs& a, const WsJob* J, Ws
                 else a.out_short[q] = nc < K ? 1 : 0;
             }
             __syncwarp();
-            for (int i = lane; i < 2 * K; i += 32) qlist[i] = ~0ull;
+            if (tk.priv) {
+                for (int i = lane; i < WS_SW * K; i += 32)
+                    lists[(size_t)(i / K) * WS_NQS * K + (size_t)qs * K + (i % K)] = ~0ull;
+            } else {
+                u64* qlist = lists + (size_t)qs * 2 * K;
+                for (int i = lane; i < 2 * K; i += 32) qlist[i] = ~0ull;
+            }
             __syncwarp();
             if (lane == 0) {
                 S->tau = ~0ull;
                 S->cur = 0;
                 S->done = 0;
+                __threadfence_block();
                 mbar_arrive(qfree + qs);  // release: state free
             }
         }
@@ -941,14 +1010,13 @@ __device__ void ws_scanner(const ScanArgs& a, WsJob* jobs, int* cnt, u64* full, 
             upk2(acc, r0, r1);
             const int qs = cur.qs;
             WsQuery* S = qst + qs;
-            u64* qlist = lists + (size_t)qs * 2 * K;
             const u64 tau = *(volatile u64*)&S->tau;
             const u64 k0 = ((u64)__float_as_uint(lut_finish<DT>(r0)) << 32) | idA;
             const u64 k1 = ((u64)__float_as_uint(lut_finish<DT>(r1)) << 32) | idB;
             tk.offer(k0, lane < cur.nb0 && k0 < tau);
-            if (tk.n > WS_WBUF - 32) tk.flush(S, qlist, K);
+            if (tk.n > WS_WBUF - 32) tk.flush(S, lists, qs, K);
             tk.offer(k1, lane < cur.nb1 && k1 < tau);
-            if (tk.n > WS_WBUF - 32) tk.flush(S, qlist, K);
+            if (tk.n > WS_WBUF - 32) tk.flush(S, lists, qs, K);
         }
         if (!hn) {
             have = false;
@@ -1110,7 +1178,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
     if ((smem_addr(lut_all) & 255u) != 0u) __trap();  // PRMT LUT addressing needs 256-byte alignment
 
     // ---- setup
-    for (int i = threadIdx.x; i < NQS * 2 * K; i += blockDim.x) lists[i] = ~0ull;
+    for (int i = threadIdx.x; i < (K <= WS_PRIV_K ? WS_SW * NQS * K : NQS * 2 * K); i += blockDim.x) lists[i] = ~0ull;
     if (threadIdx.x < WS_NQS) {
         WsQuery* S = qst + threadIdx.x;
         S->tau = ~0ull;
@@ -1231,7 +1299,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
 
         const int sw = warp - WS_BW;
         u64* wb = reinterpret_cast<u64*>(smem + L.wbuf) + (size_t)sw * 2 * WS_WBUF;
-        WarpTopK tk{wb, wb + WS_WBUF, 0};
+        WarpTopK tk{wb, wb + WS_WBUF, 0, K <= WS_PRIV_K ? lists + (size_t)sw * WS_NQS * K : nullptr};
         ws_scanner<DT, LOGN, NCH>(a, jobs, reinterpret_cast<int*>(smem + L.cnt), full, NBUF, qst, lists, K,
                                   smem_addr(lut_all), (uint32_t)(G * lut_each), (uint32_t)lut_each, tk,
                                   reinterpret_cast<u64*>(smem + L.qfree), lane);

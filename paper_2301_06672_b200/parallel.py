@@ -24,22 +24,40 @@ import numpy as np
 
 from . import _lib
 
-__all__ = ["shard_lists", "sharded_search", "CudaShardOps"]
+__all__ = ["shard_lists", "probe_frequency", "sharded_search", "CudaShardOps"]
 
 
-def shard_lists(list_len: np.ndarray, s: int, world: int) -> list[np.ndarray]:
-    """Greedy largest-first partition of lists by code bytes (L_c * s),
-    balanced over `world` ranks.  Deterministic: ties by lower list id, then
-    lower rank.  Returns the sorted list ids of every rank."""
+def shard_lists(list_len: np.ndarray, s: int, world: int, probe_freq: np.ndarray | None = None) -> list[np.ndarray]:
+    """Greedy largest-first partition of lists balanced over `world` ranks.
+    Load of list c = its code bytes L_c * s, times its probe frequency when
+    `probe_freq` is given (the scan work a rank gets is the code bytes of its
+    lists weighted by how often they are probed).  Deterministic: ties by
+    lower list id, then lower rank.  Returns the sorted list ids per rank."""
     list_len = np.asarray(list_len, dtype=np.int64)
-    order = np.lexsort((np.arange(list_len.size), -list_len))
-    load = np.zeros(world, dtype=np.int64)
+    w = list_len.astype(np.float64) * s
+    if probe_freq is not None:
+        w = w * np.asarray(probe_freq, dtype=np.float64)
+    w = w + 1.0
+    order = np.lexsort((np.arange(list_len.size), -w))
+    load = np.zeros(world, dtype=np.float64)
     owner = np.empty(list_len.size, dtype=np.int64)
     for c in order:
         r = int(np.argmin(load))  # first minimum -> lowest rank on ties
         owner[c] = r
-        load[r] += int(list_len[c]) * s + 1
+        load[r] += w[c]
     return [np.flatnonzero(owner == r).astype(np.int32) for r in range(world)]
+
+
+def probe_frequency(idx, sample: np.ndarray, nprobe: int) -> np.ndarray:
+    """How often each list is probed by `sample` (e.g. base rows, which
+    follow the query distribution) under the product's K1 -> counts [nlist]."""
+    from .index import device_index
+    sample = np.ascontiguousarray(sample, dtype=np.float32)
+    probes = np.empty((sample.shape[0], nprobe), dtype=np.int64)
+    h = device_index(idx)
+    _lib.check(_lib.lib.ivfpq_select_clusters(h.handle, sample.ctypes.data, sample.shape[0], nprobe,
+                                              probes.ctypes.data))
+    return np.bincount(probes.ravel(), minlength=idx.nlist).astype(np.float64)
 
 
 def sharded_search(ops, queries, k: int, nprobe: int, precision: str, all_gather):
