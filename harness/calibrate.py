@@ -39,9 +39,11 @@ def main():
         t0 = time.time()
         cfg_n = dict(cfg, nq=a.nq)
         base, queries = W.make_data(cfg_n)
+        td = time.time()
         arr = W.build_arrays(cfg, base, "gpu")
         t1 = time.time()
         gt = W.ground_truth_gpu(base, queries, 10)
+        print(f"[cal] data {td - t0:.1f}s build {t1 - td:.1f}s gt {time.time() - t1:.1f}s", file=sys.stderr, flush=True)
         del base
         idx = W.to_index(arr, cfg["p"])
         list_of = np.empty(cfg["n"], dtype=np.int64)

@@ -27,20 +27,25 @@ if ROOT not in sys.path:
 
 from harness import cpu_build  # noqa: E402  (numpy only)
 
-# BASELINE.json configs; generator (comps, spread) per SURVEY.md 8(d), calibrated
-# per config (profiles/r02_calibration.txt)
+# BASELINE.json configs; generator (comps, spread) per SURVEY.md 8(d); cfg3 and
+# cfg5 re-calibrated with harness/calibrate.py (profiles/r02_calibration_*.jsonl):
+# the SURVEY proposals (64 / 1024 components, spread 0.3) put recall@10 at
+# 0.46 (cfg3 p8), 0.20 (cfg3 p5), 0.60 (cfg5) -- PQ-limited, not IVF-limited.
+# ~15 points per component (cfg3: 65536 comps, spread 0.15; cfg5: 6.55M comps,
+# spread 0.1) keeps the IVF ceiling responsive to nprobe and lifts recall@10
+# at the headline nprobe to ~0.83 (cfg3 p8), 0.78 (cfg3 p5), 0.84 (cfg5).
 CONFIGS = {
     "cfg1": dict(n=100_000, d=128, nlist=1024, s=64, p=8, nq=1_000, nprobe=32, k=10, comps=16, spread=0.3, seed=1),
     "cfg2": dict(n=1_000_000, d=128, nlist=4096, s=64, p=8, nq=10_000, nprobe=32, k=10, comps=64, spread=0.3,
                  seed=2),
-    "cfg3p8": dict(n=1_000_000, d=960, nlist=4096, s=240, p=8, nq=10_000, nprobe=32, k=10, comps=64, spread=0.3,
-                   seed=3),
-    "cfg3p5": dict(n=1_000_000, d=960, nlist=4096, s=240, p=5, nq=10_000, nprobe=32, k=10, comps=64, spread=0.3,
-                   seed=3),
+    "cfg3p8": dict(n=1_000_000, d=960, nlist=4096, s=240, p=8, nq=10_000, nprobe=32, k=10, comps=65536,
+                   spread=0.15, seed=3),
+    "cfg3p5": dict(n=1_000_000, d=960, nlist=4096, s=240, p=5, nq=10_000, nprobe=32, k=10, comps=65536,
+                   spread=0.15, seed=3),
     "cfg4": dict(n=10_000_000, d=96, nlist=16384, s=48, p=8, nq=10_000, nprobe=32, k=100, comps=256, spread=0.3,
                  seed=4),
-    "cfg5": dict(n=100_000_000, d=96, nlist=65536, s=32, p=8, nq=10_000, nprobe=64, k=10, comps=1024, spread=0.3,
-                 seed=5),
+    "cfg5": dict(n=100_000_000, d=96, nlist=65536, s=32, p=8, nq=10_000, nprobe=64, k=10, comps=6_553_600,
+                 spread=0.1, seed=5),
 }
 DEFAULT_BUILDER = {"cfg1": "cpu", "cfg2": "cpu"}
 

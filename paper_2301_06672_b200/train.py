@@ -55,10 +55,14 @@ def train_pq_gpu(res, s: int, p: int, seed: int, iters: int = 12):
     g = torch.Generator(device=res.device).manual_seed(seed)
     pick = torch.randperm(n, generator=g, device=res.device)[:K]
     centers = res[pick].reshape(K, s, sub).transpose(0, 1).contiguous()   # (s, K, sub)
+    x3 = res.reshape(n, s, sub)
+    sub_id = torch.arange(s, device=res.device)[None, :] * K
     for _ in range(iters):
         codes = pq_encode_device(res, centers, p).long()                   # (n, s)
-        centers = torch.stack([_means(res[:, j * sub:(j + 1) * sub], codes[:, j], K, centers[j])
-                               for j in range(s)]).contiguous()
+        # all subspaces at once: segment means over the (subspace, code) key
+        key = (codes + sub_id).reshape(-1)
+        centers = _means(x3.reshape(n * s, sub), key, s * K, centers.reshape(s * K, sub)).reshape(s, K, sub)
+        centers = centers.contiguous()
     return centers
 
 
@@ -80,10 +84,19 @@ def build_index(data, nlist: int, s: int, p: int, seed: int = 0, train_n: int = 
     x = torch.from_numpy(X).cuda()
     g = torch.Generator(device="cuda").manual_seed(coarse_seed)
     tr = x[torch.randperm(n, generator=g, device="cuda")[:min(n, max(train_n, 8 * nlist))]].contiguous()
+    import sys
+    import time
+    t0 = time.time()
     coarse = train_coarse_gpu(tr, nlist, coarse_seed, iters)
     a, _ = assign_device(tr, coarse)
     res = (tr - coarse[a]).contiguous()
+    torch.cuda.synchronize()
+    t1 = time.time()
     centers = train_pq_gpu(res, s, p, pq_seed, iters)
     cb = PQCodebook(centers=centers.cpu().numpy(), p=p)
     del tr, res
-    return populate_lists(x, coarse.cpu().numpy(), cb)
+    t2 = time.time()
+    out = populate_lists(x, coarse.cpu().numpy(), cb)
+    print(f"[build_index] coarse {t1 - t0:.1f}s pq {t2 - t1:.1f}s populate {time.time() - t2:.1f}s", file=sys.stderr,
+          flush=True)
+    return out
