@@ -79,7 +79,7 @@ def test_cfg2_recall_fp8_within_001_of_f32(cfg2):
     rec = {}
     for prec in PRECS:
         lists, _ = pkg.search_batch(idx, q, pkg.SearchParams(k=10, nprobe=32, precision=prec))
-        rec[prec] = pkg.recall(lists, gt)[1]
+        rec[prec] = pkg.recall(lists, pkg.NeighborLists(ids=gt))[1]
     assert rec["f32"] > 0.7, rec
     assert abs(rec["f16"] - rec["f32"]) < 0.002, rec
     assert rec["f32"] - rec["e5m3"] < 0.01 and rec["f32"] - rec["e4m4"] < 0.01, rec
