@@ -3,6 +3,7 @@ headline metrics, per-region executed-instruction histogram of the SASS
 (with stall samples) and the opcode mix of the hottest regions.
 
   python harness/ncu_src.py gpurun_out/prof.ncu-rep [--kernel scan_ws] [--bucket 0x400]
+  python harness/ncu_src.py gpurun_out/<tag>          (CSVs from harness/ncu_capture.sh)
 """
 
 from __future__ import annotations
@@ -27,8 +28,17 @@ def ncu(*args) -> str:
     return subprocess.run(["ncu", *args], capture_output=True, text=True, check=True).stdout
 
 
+def _page(rep: str, page: str) -> str:
+    """A report's page as CSV text: from the .ncu-rep, or from the CSVs that
+    harness/ncu_capture.sh exported next to it (<tag>_raw.csv / <tag>_src.csv)."""
+    if rep.endswith(".ncu-rep"):
+        args = ["-i", rep, "--page", page, "--csv"] + (["--print-source", "sass"] if page == "source" else [])
+        return ncu(*args)
+    return open(f"{rep}_{'raw' if page == 'raw' else 'src'}.csv").read()
+
+
 def raw_metrics(rep: str, kernel: str) -> list[dict]:
-    rows = list(csv.reader(io.StringIO(ncu("-i", rep, "--page", "raw", "--csv"))))
+    rows = list(csv.reader(io.StringIO(_page(rep, "raw"))))
     hdr = rows[0]
     out = []
     for r in rows[2:]:
@@ -56,7 +66,7 @@ def main():
         tot = sum(st.values()) or 1.0
         top = sorted(st.items(), key=lambda kv: -kv[1])[:10]
         print("   stalls: " + ", ".join(f"{k.split('stalled_')[-1]} {v / tot * 100:.1f}%" for k, v in top))
-    src = list(csv.reader(io.StringIO(ncu("-i", a.rep, "--page", "source", "--csv", "--print-source", "sass"))))
+    src = list(csv.reader(io.StringIO(_page(a.rep, "source"))))
     hdr = src[1]
     iI = hdr.index("Instructions Executed")
     iS = hdr.index("Warp Stall Sampling (All Samples)")
