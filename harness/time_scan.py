@@ -29,12 +29,14 @@ def main():
         idx = IvfPqIndex.from_csr(z["coarse"], PQCodebook(centers=z["centers"], p=cfg["p"]), z["off"], z["ids"],
                                   z["codes"])
         queries = z["queries"]
+        del z
     else:
         base, queries = W.make_data(cfg)
-        idx = W.build_index_gpu(base, cfg["nlist"], cfg["s"], cfg["p"], seed=cfg["seed"])
+        arr = W.build_arrays(cfg, base, W.DEFAULT_BUILDER.get(a.config, "gpu"))   # the bench's index
         del base
-        off, ids, codes = idx.csr()
-        np.savez(cache, coarse=idx.coarse, centers=idx.cb.centers, off=off, ids=ids, codes=codes, queries=queries)
+        idx = W.to_index(arr, cfg["p"])
+        np.save(cache.replace(".npz", "_q.npy"), queries)
+        np.savez(cache, queries=queries, **arr)
     dev = DeviceIndex(idx, 0)
     q = torch.from_numpy(queries).cuda()
     k, P = cfg["k"], a.nprobe or cfg["nprobe"]

@@ -228,6 +228,10 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
                  : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// Bulk L2 prefetch of a contiguous global range (16-byte aligned, multiple of 16 bytes).
+__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ uint4 lds128(uint32_t a) {
     uint4 r;
     asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(a));
@@ -1278,6 +1282,14 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
                 if (lane == 0) mbar_arrive(full + slot);
                 break;
             }
+            // The job's code ranges (one contiguous range per list in the
+            // interleaved layout) are pulled into L2 now, a job or more before
+            // the scanners reach them: when the code store is larger than L2
+            // (cfg5: 3.2 GB) the scanners' own register prefetch of one pair
+            // ahead cannot cover the DRAM latency.
+#ifndef WS_NO_L2PF  // (variant switch for experiments)
+            if (t < PJ->ng) prefetch_l2(a.codes + PJ->off[t] * a.s_pad, (uint32_t)PJ->len[t] * (uint32_t)a.s_pad);
+#endif
             B.build(reinterpret_cast<const uint8_t*>(prq) + (size_t)ps * G * d_pad * 4, (uint32_t)(d_pad * 4),
                     lut_all + (size_t)slot * G * lut_each, (uint32_t)lut_each, PJ->ng, jpt);
             __syncwarp();  // the warp's LUT stores / prep reads are ordered before its arrivals
