@@ -124,6 +124,7 @@ struct ivfpq_index {
     // scratch
     DevBuf q, dist, pkeys, oids, odist, oshort, keys, ncand, work, plan_jobs, plan_rq, plan_nj, plan_nc, tc_sl, flags, glut;
     int num_sms = 0;
+    int64_t l2_bytes = 0;  // device L2 size (scan: bulk L2 prefetch when the code store exceeds it)
 };
 
 namespace {
@@ -616,6 +617,7 @@ int run_scan(ivfpq_index* idx, const float* d_q, int64_t nq, const uint64_t* d_p
         w.a = a;
         w.NBUF = plan.NBUF;
         w.gmem = plan.gmem;
+        w.l2pf = (int64_t)idx->n_local * idx->s_pad > idx->l2_bytes ? 1 : 0;
         CKR(idx->work.ensure(16));
         w.work = idx->work.as<int>();
         CK(cudaMemsetAsync(w.work, 0, sizeof(int), st));
@@ -811,6 +813,11 @@ int ivfpq_index_create(int device, const float* coarse, int64_t nlist, int64_t d
     CKI(cudaStreamCreateWithFlags(&idx->stream, cudaStreamNonBlocking));
     CKI(cudaEventCreateWithFlags(&idx->last_ev, cudaEventDisableTiming));
     CKI(cudaDeviceGetAttribute(&idx->num_sms, cudaDevAttrMultiProcessorCount, device));
+    {
+        int l2 = 0;
+        CKI(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device));
+        idx->l2_bytes = l2;
+    }
     auto up = [&](void** dst, const void* src, size_t bytes) -> cudaError_t {
         cudaError_t e = cudaMalloc(dst, std::max<size_t>(bytes, 16));
         if (e != cudaSuccess) return e;
@@ -1360,6 +1367,11 @@ int ivfpq_knn_create(int device, const float* base, int64_t n, int64_t d, ivfpq_
     CKI(cudaStreamCreateWithFlags(&idx->stream, cudaStreamNonBlocking));
     CKI(cudaEventCreateWithFlags(&idx->last_ev, cudaEventDisableTiming));
     CKI(cudaDeviceGetAttribute(&idx->num_sms, cudaDevAttrMultiProcessorCount, device));
+    {
+        int l2 = 0;
+        CKI(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device));
+        idx->l2_bytes = l2;
+    }
     CKI(cudaMalloc((void**)&idx->coarse, (size_t)n * d * 4));
     CKI(cudaMemcpy(idx->coarse, base, (size_t)n * d * 4, cudaMemcpyHostToDevice));
     std::vector<int32_t> ident(n);

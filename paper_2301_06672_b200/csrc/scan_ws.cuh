@@ -85,6 +85,7 @@ struct WsArgs {
     int JMAX;
     int NBUF;
     int gmem;              // 1: builders read the codebook from global memory (does not fit TMEM)
+    int l2pf;              // 1: builders bulk-prefetch each job's codes into L2 (code store > L2)
     int* work;             // global query counter (zeroed before launch)
 };
 
@@ -1282,14 +1283,14 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
                 if (lane == 0) mbar_arrive(full + slot);
                 break;
             }
-            // The job's code ranges (one contiguous range per list in the
-            // interleaved layout) are pulled into L2 now, a job or more before
-            // the scanners reach them: when the code store is larger than L2
-            // (cfg5: 3.2 GB) the scanners' own register prefetch of one pair
-            // ahead cannot cover the DRAM latency.
-#ifndef WS_NO_L2PF  // (variant switch for experiments)
-            if (t < PJ->ng) prefetch_l2(a.codes + PJ->off[t] * a.s_pad, (uint32_t)PJ->len[t] * (uint32_t)a.s_pad);
-#endif
+            // When the code store is larger than L2 (cfg5: 3.2 GB) the job's
+            // code ranges (one contiguous range per list in the interleaved
+            // layout) are pulled into L2 now, a job or more before the scanners
+            // reach them: their own register prefetch of one pair ahead does not
+            // cover the DRAM latency (cfg5 e5m3 scan 47.1 -> 44.5 ms; with an
+            // L2-resident store it only adds requests: cfg2 +1.7%, so off there).
+            if (w.l2pf && t < PJ->ng)
+                prefetch_l2(a.codes + PJ->off[t] * a.s_pad, (uint32_t)PJ->len[t] * (uint32_t)a.s_pad);
             B.build(reinterpret_cast<const uint8_t*>(prq) + (size_t)ps * G * d_pad * 4, (uint32_t)(d_pad * 4),
                     lut_all + (size_t)slot * G * lut_each, (uint32_t)lut_each, PJ->ng, jpt);
             __syncwarp();  // the warp's LUT stores / prep reads are ordered before its arrivals
