@@ -49,15 +49,10 @@ def main():
     cfg = W.CONFIGS[a.config]
     t0 = time.time()
     base, queries = W.make_data(cfg)
+    arr = W.build_arrays(cfg, base, W.DEFAULT_BUILDER.get(a.config, "gpu"))
     # probe-frequency proxy from base rows (same distribution as the queries,
     # disjoint from them): 20K rows
     pseudo = base[np.random.default_rng(1).choice(base.shape[0], 20_000, replace=False)]
-    cache = f"/tmp/ivfpq_ts_{a.config}.npz"      # harness/time_scan.py's index of the same call, if any
-    if os.path.exists(cache):
-        z = np.load(cache)
-        arr = {k: z[k] for k in ("coarse", "centers", "off", "ids", "codes")}
-    else:
-        arr = W.build_arrays(cfg, base, W.DEFAULT_BUILDER.get(a.config, "gpu"))
     del base
     idx = W.to_index(arr, cfg["p"])
     lens = np.diff(arr["off"])

@@ -769,7 +769,6 @@ struct WsPair {
     const uint8_t* p0;
     const uint8_t* p1;
     uint32_t st0, st1;
-    uint32_t id0, id1;      // this lane's vector ids in each block
 };
 
 // A job's list table held lane-parallel (lane g < ng describes list g), read
@@ -940,28 +939,40 @@ __device__ void ws_scanner(const ScanArgs& a, WsJob* jobs, int* cnt, u64* full, 
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
     const uint8_t* codes = a.codes;
     uint4 A[NS], B[NS];
+    uint32_t idA = 0, idB = 0;
     int slot = 0, ph = 0;
-    WsPair P0, P1;
+    WsPair cur, nxt;
     WsJobTab ct, nt;
     mbar_wait(full, 0);
     if (jobs[0].qs < 0) return;
     ct.load(jobs, lane);
-    bool have = ws_grab(ct, cnt, 0, lut_s0, lut_each, codes, s_pad, lane, P0);
-    auto load_first = [&](WsPair& p) {
+    bool have = ws_grab(ct, cnt, 0, lut_s0, lut_each, codes, s_pad, lane, cur);
+    auto load_first = [&](const WsPair& p) {
 #pragma unroll
         for (int u = 0; u < NS; ++u)
             if (u < nch) {
                 A[u] = ws_ld(p.p0 + u * p.st0, pol);
                 B[u] = ws_ld(p.p1 + u * p.st1, pol);
             }
-        p.id0 = lane < p.nb0 ? __ldg(a.ids + p.vo0 + lane) : 0u;
-        p.id1 = lane < p.nb1 ? __ldg(a.ids + p.vo1 + lane) : 0u;
+        idA = lane < p.nb0 ? __ldg(a.ids + p.vo0 + lane) : 0u;
+        idB = lane < p.nb1 ? __ldg(a.ids + p.vo1 + lane) : 0u;
     };
-    // One pair: grab the next pair (same job, else the next job if its LUTs
-    // are ready), scan `cur` while refilling the chunk registers with `nxt`,
-    // offer.  Returns false when there is no next pair.  Called with the two
-    // pair registers in alternating roles (below), so a pair is never copied.
-    auto step = [&](WsPair& cur, WsPair& nxt) -> bool {
+    if (have) load_first(cur);
+    while (true) {
+        if (!have) {
+            ws_job_end(a, jobs + slot, qst, lists, K, tk, qfree, slot, lane);
+            if (++slot == NBUF) {
+                slot = 0;
+                ph ^= 1;
+            }
+            mbar_wait(full + slot, ph);
+            if (jobs[slot].qs < 0) break;
+            ct.load(jobs + slot, lane);
+            have = ws_grab(ct, cnt, slot, lut_s0 + (uint32_t)slot * slot_bytes, lut_each, codes, s_pad, lane, cur);
+            if (have) load_first(cur);
+            continue;
+        }
+        // ---- the next pair: same job, else the next job if its LUTs are ready
         bool hn = ws_grab(ct, cnt, slot, lut_s0 + (uint32_t)slot * slot_bytes, lut_each, codes, s_pad, lane, nxt);
         bool cross = false;
         if (!hn) {
@@ -979,10 +990,8 @@ __device__ void ws_scanner(const ScanArgs& a, WsJob* jobs, int* cnt, u64* full, 
         const uint8_t* n0 = hn ? nxt.p0 : cur.p0;
         const uint8_t* n1 = hn ? nxt.p1 : cur.p1;
         const uint32_t ns0 = hn ? nxt.st0 : cur.st0, ns1 = hn ? nxt.st1 : cur.st1;
-        if (hn) {
-            nxt.id0 = lane < nxt.nb0 ? __ldg(a.ids + nxt.vo0 + lane) : 0u;
-            nxt.id1 = lane < nxt.nb1 ? __ldg(a.ids + nxt.vo1 + lane) : 0u;
-        }
+        const uint32_t nidA = hn && lane < nxt.nb0 ? __ldg(a.ids + nxt.vo0 + lane) : 0u;
+        const uint32_t nidB = hn && lane < nxt.nb1 ? __ldg(a.ids + nxt.vo1 + lane) : 0u;
         // ---- scan the current pair
         const uint32_t base0 = cur.base0, base1 = cur.base1;
         u64 acc = pk2(0.f, 0.f);
@@ -1007,14 +1016,18 @@ __device__ void ws_scanner(const ScanArgs& a, WsJob* jobs, int* cnt, u64* full, 
             const int qs = cur.qs;
             WsQuery* S = qst + qs;
             const u64 tau = *(volatile u64*)&S->tau;
-            const u64 k0 = ((u64)__float_as_uint(lut_finish<DT>(r0)) << 32) | cur.id0;
-            const u64 k1 = ((u64)__float_as_uint(lut_finish<DT>(r1)) << 32) | cur.id1;
+            const u64 k0 = ((u64)__float_as_uint(lut_finish<DT>(r0)) << 32) | idA;
+            const u64 k1 = ((u64)__float_as_uint(lut_finish<DT>(r1)) << 32) | idB;
             tk.offer(k0, lane < cur.nb0 && k0 < tau);
             if (tk.n > WS_WBUF - 32) tk.flush(S, lists, qs, K);
             tk.offer(k1, lane < cur.nb1 && k1 < tau);
             if (tk.n > WS_WBUF - 32) tk.flush(S, lists, qs, K);
         }
-        if (hn && cross) {  // this warp's part of the current job is done
+        if (!hn) {
+            have = false;
+            continue;
+        }
+        if (cross) {  // this warp's part of the current job is done
             ws_job_end(a, jobs + slot, qst, lists, K, tk, qfree, slot, lane);
             if (++slot == NBUF) {
                 slot = 0;
@@ -1022,31 +1035,9 @@ __device__ void ws_scanner(const ScanArgs& a, WsJob* jobs, int* cnt, u64* full, 
             }
             ct = nt;
         }
-        return hn;
-    };
-    if (have) load_first(P0);
-    while (true) {
-        if (!have) {
-            ws_job_end(a, jobs + slot, qst, lists, K, tk, qfree, slot, lane);
-            if (++slot == NBUF) {
-                slot = 0;
-                ph ^= 1;
-            }
-            mbar_wait(full + slot, ph);
-            if (jobs[slot].qs < 0) break;
-            ct.load(jobs + slot, lane);
-            have = ws_grab(ct, cnt, slot, lut_s0 + (uint32_t)slot * slot_bytes, lut_each, codes, s_pad, lane, P0);
-            if (have) load_first(P0);
-            continue;
-        }
-        if (!step(P0, P1)) {  // P0 current; on success P1 is
-            have = false;
-            continue;
-        }
-        if (!step(P1, P0)) {
-            have = false;     // (the blocking path refills P0)
-            continue;
-        }
+        cur = nxt;
+        idA = nidA;
+        idB = nidB;
     }
 }
 
