@@ -44,15 +44,20 @@ def main():
     a = ap.parse_args()
     import torch
     from harness import workload as W
-    from paper_2301_06672_b200 import parallel
+    from paper_2301_06672_b200 import _lib, parallel
     from paper_2301_06672_b200.index import DeviceIndex
     cfg = W.CONFIGS[a.config]
     t0 = time.time()
     base, queries = W.make_data(cfg)
-    arr = W.build_arrays(cfg, base, W.DEFAULT_BUILDER.get(a.config, "gpu"))
     # probe-frequency proxy from base rows (same distribution as the queries,
     # disjoint from them): 20K rows
     pseudo = base[np.random.default_rng(1).choice(base.shape[0], 20_000, replace=False)]
+    cache = f"/tmp/ivfpq_ts_{a.config}.npz"      # harness/time_scan.py's index of the same call, if any
+    if os.path.exists(cache):
+        z = np.load(cache)
+        arr = {k: z[k] for k in ("coarse", "centers", "off", "ids", "codes")}
+    else:
+        arr = W.build_arrays(cfg, base, W.DEFAULT_BUILDER.get(a.config, "gpu"))
     del base
     idx = W.to_index(arr, cfg["p"])
     lens = np.diff(arr["off"])
@@ -84,12 +89,20 @@ def main():
         return full.finalize(sk, nc, k)
 
     t1, ref = timed(single)
+    n1 = _lib.ctypes.c_int64()
+    _lib.check(_lib.lib.ivfpq_debug_select_flagged(full.dev.handle, _lib.ctypes.byref(n1)))
+    print(f"[shard] T1 {t1:.3f} ms, K1 guard re-dos {n1.value}", file=sys.stderr, flush=True)
     ref_ids, ref_d = ref[0].cpu().numpy(), ref[1].cpu().numpy()
     for world in a.world:
         shards = parallel.shard_lists(lens, cfg["s"], world, freq)
         ops = [parallel.CudaShardOps(DeviceIndex(idx, 0, owned=sh)) for sh in shards]
         # stage 1: local K1 per shard, then the (replicated) probe merge
         sel = [timed(lambda o=o: o.select(qd, P)) for o in ops]
+        flagged = []
+        for o in ops:   # queries the tensor-core K1 guard sent to the exact SIMT re-do, per shard
+            n = _lib.ctypes.c_int64()
+            _lib.check(_lib.lib.ivfpq_debug_select_flagged(o.dev.handle, _lib.ctypes.byref(n)))
+            flagged.append(int(n.value))
         stacked = torch.stack([s[1] for s in sel])
         t_merge_p, probes = timed(lambda: ops[0].merge(stacked, P))
         # stage 2: local scans, then the (replicated) top-k merge + finalize
@@ -105,7 +118,8 @@ def main():
         owned_bytes = [int(lens[sh].sum()) * cfg["s"] for sh in shards]
         row = {"config": a.config, "world": world, "dtype": a.dtype, "balance": a.balance,
                "t1_ms": round(t1, 3), "t_shard_ms": [round(x, 3) for x in per],
-               "select_ms": [round(s[0], 3) for s in sel], "scan_ms": [round(c[0], 3) for c in scans],
+               "select_ms": [round(s[0], 3) for s in sel], "select_flagged": flagged,
+               "scan_ms": [round(c[0], 3) for c in scans],
                "merge_probes_ms": round(t_merge_p, 3), "merge_topk_ms": round(t_merge_k + t_fin, 3),
                "allgather_bytes_per_rank": ag_bytes, "allgather_est_ms": round(t_ag, 3),
                "owned_code_bytes": owned_bytes,

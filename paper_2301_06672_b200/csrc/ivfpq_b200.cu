@@ -193,6 +193,59 @@ __global__ void merge_keys_kernel(const uint64_t* __restrict__ in, int W, int nq
     }
 }
 
+// Merge of W ascending key runs per row ([W][nq][n_in] -> [nq][n_out]) by a
+// tree of pairwise merge-paths in shared memory, one warp per row: the
+// multi-GPU protocol's two merges (probe keys, top-k keys) get rows that are
+// already sorted by the ranks, so no selection is needed.  Equal keys (only
+// the UINT64_MAX padding) are placed by lower / upper bounds: every output
+// slot is written exactly once.
+constexpr int MS_WARPS = 4;
+__global__ void __launch_bounds__(32 * MS_WARPS) merge_sorted_kernel(const uint64_t* __restrict__ in, int W, int nq,
+                                                                     int n_in, int n_out, uint64_t* __restrict__ out) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int row = blockIdx.x * MS_WARPS + warp;
+    if (row >= nq) return;
+    const int cap = W * n_in;
+    uint64_t* buf = reinterpret_cast<uint64_t*>(smem) + (size_t)warp * 2 * cap;
+    uint64_t* cur = buf;
+    uint64_t* nxt = buf + cap;
+    for (int i = lane; i < cap; i += 32) {
+        const int w = i / n_in, j = i - w * n_in;
+        cur[i] = in[((size_t)w * nq + row) * n_in + j];
+    }
+    // runs r = 0..nr-1 of length len (the last run may be shorter after truncation)
+    int nr = W, len = n_in;
+    __syncwarp();
+    while (nr > 1) {
+        const int olen = min(2 * len, max(n_out, len));   // merged run length kept
+        const int np = (nr + 1) / 2;
+        for (int r = 0; r < np; ++r) {
+            const uint64_t* A = cur + (size_t)(2 * r) * len;
+            uint64_t* O = nxt + (size_t)r * olen;
+            if (2 * r + 1 < nr) {
+                const uint64_t* B = A + len;
+                for (int i = lane; i < len; i += 32) {
+                    const int pa = i + lower_bound_u64(B, len, A[i]);
+                    if (pa < olen) O[pa] = A[i];
+                    const int pb = i + upper_bound_u64(A, len, B[i]);
+                    if (pb < olen) O[pb] = B[i];
+                }
+                for (int i = 2 * len + lane; i < olen; i += 32) O[i] = ~0ull;  // (olen <= 2 len)
+            } else {
+                for (int i = lane; i < olen; i += 32) O[i] = i < len ? A[i] : ~0ull;
+            }
+        }
+        __syncwarp();
+        uint64_t* t = cur;
+        cur = nxt;
+        nxt = t;
+        nr = np;
+        len = olen;
+    }
+    for (int i = lane; i < n_out; i += 32) out[(size_t)row * n_out + i] = i < len ? cur[i] : ~0ull;
+}
+
 __global__ void finalize_kernel(const uint64_t* __restrict__ keys, const int64_t* __restrict__ ncand, int nq, int K,
                                 int64_t* __restrict__ ids, float* __restrict__ dists, int32_t* __restrict__ shrt) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -940,6 +993,17 @@ int ivfpq_merge_keys_device(const uint64_t* d_in, int64_t W, int64_t nq, int64_t
         return set_err(IVFPQ_EINVAL, "invalid merge shape W=%lld n_in=%lld n_out=%lld", (long long)W,
                        (long long)n_in, (long long)n_out);
     if (nq == 0) return IVFPQ_OK;
+    // rows arrive sorted (the contract): pairwise merge-paths, one warp per row,
+    // when the runs fit shared memory; else the block top-k selection
+    const size_t ms_smem = (size_t)MS_WARPS * 2 * W * n_in * 8;
+    if (ms_smem <= SMEM_LIMIT) {
+        CKR(set_smem_attr((const void*)merge_sorted_kernel, ms_smem));
+        merge_sorted_kernel<<<(unsigned)((nq + MS_WARPS - 1) / MS_WARPS), 32 * MS_WARPS, ms_smem,
+                              reinterpret_cast<cudaStream_t>(stream)>>>(d_in, (int)W, (int)nq, (int)n_in, (int)n_out,
+                                                                        d_out);
+        KCHECK();
+        return IVFPQ_OK;
+    }
     CKR(set_smem_attr((const void*)merge_keys_kernel, SMEM_LIMIT));  // per-device: set every launch
     merge_keys_kernel<<<(unsigned)nq, TK_BLOCK, topk_smem((int)n_out), reinterpret_cast<cudaStream_t>(stream)>>>(
         d_in, (int)W, (int)nq, (int)n_in, (int)n_out, d_out);
