@@ -39,7 +39,7 @@ def main():
     ap.add_argument("--world", type=int, nargs="+", default=[2, 4, 8])
     ap.add_argument("--dtype", default="e5m3")
     ap.add_argument("--balance", choices=["bytes", "probe"], default="probe")
-    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--out", default="gpurun_out/shard_emulate.jsonl")
     a = ap.parse_args()
     import torch
@@ -120,7 +120,8 @@ def main():
                "t1_ms": round(t1, 3), "t_shard_ms": [round(x, 3) for x in per],
                "select_ms": [round(s[0], 3) for s in sel], "select_flagged": flagged,
                "scan_ms": [round(c[0], 3) for c in scans],
-               "merge_probes_ms": round(t_merge_p, 3), "merge_topk_ms": round(t_merge_k + t_fin, 3),
+               "merge_probes_ms": round(t_merge_p, 3), "merge_topk_ms": round(t_merge_k, 3),
+               "finalize_ms": round(t_fin, 3),
                "allgather_bytes_per_rank": ag_bytes, "allgather_est_ms": round(t_ag, 3),
                "owned_code_bytes": owned_bytes,
                "emulated_speedup": round(t1 / (max(per) + t_ag), 3), "bit_identical_to_1gpu": exact}

@@ -1289,7 +1289,11 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
             // reach them: their own register prefetch of one pair ahead does not
             // cover the DRAM latency (cfg5 e5m3 scan 47.1 -> 44.5 ms; with an
             // L2-resident store it only adds requests: cfg2 +1.7%, so off there).
+#ifdef WS_NO_L2PF  // (variant switch for experiments)
+            if (false)
+#else
             if (w.l2pf && t < PJ->ng)
+#endif
                 prefetch_l2(a.codes + PJ->off[t] * a.s_pad, (uint32_t)PJ->len[t] * (uint32_t)a.s_pad);
             B.build(reinterpret_cast<const uint8_t*>(prq) + (size_t)ps * G * d_pad * 4, (uint32_t)(d_pad * 4),
                     lut_all + (size_t)slot * G * lut_each, (uint32_t)lut_each, PJ->ng, jpt);
