@@ -1,6 +1,6 @@
 """8-GPU readiness on ONE B200 (only one GPU is reachable here): the
 list-sharded protocol of parallel.py with W shards held as W device handles
-on the same GPU, each shard's work timed ALONE (CUDA events, L2 flushed):
+on the same GPU, each shard's work timed ALONE (CUDA events, L2 flushed, median of 7):
 
   T_shard(r) = local K1 (select over owned centroids) + probe merge
              + local scan of the owned probed lists + top-k merge + finalize
@@ -39,7 +39,7 @@ def main():
     ap.add_argument("--world", type=int, nargs="+", default=[2, 4, 8])
     ap.add_argument("--dtype", default="e5m3")
     ap.add_argument("--balance", choices=["bytes", "probe"], default="probe")
-    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--reps", type=int, default=7)
     ap.add_argument("--out", default="gpurun_out/shard_emulate.jsonl")
     a = ap.parse_args()
     import torch
@@ -79,7 +79,7 @@ def main():
             e1.record()
             e1.synchronize()
             ts.append(e0.elapsed_time(e1))
-        return float(np.mean(ts)), out
+        return float(np.median(ts)), out   # median: robust to the sporadic ~2 ms stalls seen on the box
 
     full = parallel.CudaShardOps(DeviceIndex(idx, 0))
 

@@ -39,6 +39,21 @@
 
 namespace ivfpq {
 
+// Checked build (-DIVFPQ_CHECKED, harness/checked_run.sh): device-side bounds
+// and protocol assertions that trap on violation.  compute-sanitizer is closed
+// on this GPU pool, so this build plus the CPU-oracle parity tests stand in for
+// memcheck / racecheck.  Compiled out of the product library.
+#ifdef IVFPQ_CHECKED
+#define WS_CHECK(cond)          \
+    do {                        \
+        if (!(cond)) __trap();  \
+    } while (0)
+#else
+#define WS_CHECK(cond) \
+    do {               \
+    } while (0)
+#endif
+
 #ifndef WS_BW_CFG
 #define WS_BW_CFG 8
 #define WS_SW_CFG 11
@@ -608,6 +623,7 @@ struct WarpTopK {
 
     __device__ __forceinline__ void offer(u64 key, bool pred) {
         const unsigned m = __ballot_sync(0xffffffffu, pred);
+        WS_CHECK(n + __popc(m) <= WS_WBUF);
         if (pred) buf[n + __popc(m & ((1u << (threadIdx.x & 31)) - 1))] = key;
         n += __popc(m);
     }
@@ -788,6 +804,7 @@ struct WsJobTab {
     }
     __device__ __forceinline__ void block(int b, int& g, int& nb, int& vo) const {
         const unsigned m = __ballot_sync(0xffffffffu, pref <= b);  // prefs ascend; pref[0] = 0
+        WS_CHECK(m != 0u && b >= 0 && b < nblk);
         g = 31 - __clz(m);
         const int pg = __shfl_sync(0xffffffffu, pref, g);
         const int lg = __shfl_sync(0xffffffffu, len, g);
@@ -819,6 +836,7 @@ __device__ __forceinline__ bool ws_grab(const WsJobTab& T, int* cnt, int slot, u
         p.nb1 = 0;
         p.vo1 = p.vo0;
     }
+    WS_CHECK(p.nb0 >= 1 && p.nb0 <= 32 && p.nb1 >= 0 && p.nb1 <= 32 && p.vo0 >= 0 && p.vo1 >= 0);
     const int l0 = min(lane, p.nb0 - 1), l1 = min(lane, max(p.nb1 - 1, 0));
     p.p0 = codes + (long long)p.vo0 * s_pad + l0 * 16;
     p.p1 = codes + (long long)p.vo1 * s_pad + l1 * 16;
@@ -851,6 +869,7 @@ __device__ __forceinline__ void ws_job_end(const ScanArgs& a, const WsJob* J, Ws
             d = atomicAdd(&S->done, 1);
         }
         d = __shfl_sync(0xffffffffu, d, 0);
+        WS_CHECK(d >= 0 && d < WS_SW);
         if (d == WS_SW - 1) {
             __threadfence_block();
             const u64* r;
@@ -1067,6 +1086,7 @@ __global__ void __launch_bounds__(256) ws_plan_kernel(const ScanArgs a, int G, i
     int pend = 0, nj = 0;
     long long nc = 0;
     auto emit = [&](int from, int ng, bool last) {
+        WS_CHECK(nj < JMAX && ng <= G);
         WsJob* J = jobs + (size_t)q * JMAX + nj;
         if (lane == 0) {
             int pref = 0;
@@ -1268,6 +1288,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
             if (wrapped) nbar_sync(WS_BAR_EMPTY0 + slot, WS_BAR_EMPTY_N);
             const WsJob* PJ = pjobs + ps;
             const int pq_s = reinterpret_cast<const int*>(smem + L.prepq)[ps];
+            WS_CHECK(pq_s >= -1 && pq_s < WS_NQS && (pq_s < 0 || (PJ->ng >= 1 && PJ->ng <= G && PJ->nblk >= PJ->ng)));
             if (t < 32) {  // the descriptor travels with the LUT slot (warp 0 copies it)
                 const int* src = reinterpret_cast<const int*>(PJ);
                 int* dst = reinterpret_cast<int*>(jobs + slot);
