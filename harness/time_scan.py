@@ -15,6 +15,7 @@ def main():
     ap.add_argument("--dtypes", nargs="+", default=["e5m3"])
     ap.add_argument("--nprobe", type=int, default=None)
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--scan-mode", type=int, default=0, help="ivfpq_set_scan_kernel mode (2: prefer row chunks)")
     a = ap.parse_args()
     import numpy as np
     import torch
@@ -37,6 +38,7 @@ def main():
         idx = W.to_index(arr, cfg["p"])
         np.save(cache.replace(".npz", "_q.npy"), queries)
         np.savez(cache, queries=queries, **arr)
+    _lib.check(_lib.lib.ivfpq_set_scan_kernel(a.scan_mode))
     dev = DeviceIndex(idx, 0)
     q = torch.from_numpy(queries).cuda()
     k, P = cfg["k"], a.nprobe or cfg["nprobe"]
@@ -59,7 +61,8 @@ def main():
             e1.synchronize()
             if r:
                 ts.append(e0.elapsed_time(e1))
-        print(f"{a.config} {prec} nprobe {P}: scan {np.mean(ts):.3f} ms (min {np.min(ts):.3f})", flush=True)
+        print(f"{a.config} {prec} nprobe {P} mode {a.scan_mode}: scan {np.mean(ts):.3f} ms (min {np.min(ts):.3f})",
+              flush=True)
 
 
 if __name__ == "__main__":

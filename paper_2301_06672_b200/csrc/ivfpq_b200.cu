@@ -122,7 +122,9 @@ struct ivfpq_index {
     cudaStream_t last_stream = nullptr;
     bool last_used = false;
     // scratch
-    DevBuf q, dist, pkeys, oids, odist, oshort, keys, ncand, work, plan_jobs, plan_rq, plan_nj, plan_nc, tc_sl, flags, glut;
+    DevBuf q, dist, pkeys, oids, odist, oshort, keys, ncand, work, plan_jobs, plan_rq, plan_nj, plan_nc, tc_sl, flags, glut,
+        part;
+    int64_t max_len = 0;  // longest owned list (chunked scan: partial-sum scratch per warp)
     int num_sms = 0;
     int64_t l2_bytes = 0;  // device L2 size (scan: bulk L2 prefetch when the code store exceeds it)
 };
@@ -558,6 +560,7 @@ struct WsPlan {
     int G, NBUF;
     size_t smem;
     int gmem;
+    int nh = 1, rc = 0;  // row-chunked LUT jobs: nh chunks of rc rows (nh = 1: unchunked)
 };
 
 // 0 = auto (v2 when the shape fits), 1 = force v1; set by ivfpq_set_scan_kernel
@@ -592,23 +595,53 @@ bool ws_plan(const ivfpq_index* idx, int64_t P, int64_t K, int dt, WsPlan* plan)
         const char* e = getenv("IVFPQ_WS_NBUF");
         return e ? atoi(e) : 0;
     }();
-    // Preference (measured on cfg2): >= 3 LUT slots (builders and scanners
-    // decoupled by a job of slack) with the largest G >= 2 that allows them
-    // (fp8: G=3 x 3 slots, 4.86 ms vs G=4 x 2 slots, 5.18 ms), then code
-    // stages; otherwise 2 slots (f16: G=2 x 2, 6.33 ms vs G=1 x 4, 7.38 ms).
     const int G0 = G;
-    // (a single slot -- build, then scan -- is the last resort before the
-    // per-query kernel: cfg3 p8 with f16 LUTs of 120 KiB)
-    for (int min_nb = 3; min_nb >= 1; --min_nb)
-    for (G = G0; G >= (min_nb == 3 ? 2 : 1); --G)
-        for (int nb = env_nb ? env_nb : WS_MAX_NBUF; nb >= min_nb; --nb) {
-            const size_t sm = WsLayout((int)idx->d, (int)idx->s, (int)idx->sub_d, (int)idx->p, lut_bytes_of((int)dt), G,
-                                       nb, (int)K, (int)idx->s_pad).total;
-            if (sm <= SMEM_LIMIT) {
-                *plan = WsPlan{G, nb, sm, gmem ? 1 : 0};
-                return true;
-            }
+    const int esz = lut_bytes_of((int)dt);
+    auto fits = [&](int g, int nb, int rc) {
+        return WsLayout((int)idx->d, (int)idx->s, (int)idx->sub_d, (int)idx->p, esz, g, nb, (int)K, (int)idx->s_pad, rc)
+            .total;
+    };
+    // unchunked: the largest G with >= min_nb LUT slots
+    auto unchunked = [&](int min_nb, int min_g) -> bool {
+        for (int g = G0; g >= min_g; --g)
+            for (int nb = env_nb ? env_nb : WS_MAX_NBUF; nb >= min_nb; --nb)
+                if (fits(g, nb, 0) <= SMEM_LIMIT) {
+                    *plan = WsPlan{g, nb, fits(g, nb, 0), gmem ? 1 : 0};
+                    return true;
+                }
+        return false;
+    };
+    // row-chunked: rc rows per job (a multiple of 16 -- whole code chunks --
+    // and of R -- whole builder rows -- dividing s_pad), the largest rc and
+    // then G with >= min_nb slots; the lists' partial sums are carried in a
+    // per-warp scratch between the nh = s_pad / rc jobs of a group
+    auto chunked = [&](int min_nb, int min_g) -> bool {
+        if (idx->p < 5) return false;  // (row-chunked kernels are built for 2^p >= 32)
+        const int64_t step = std::max<int64_t>(16, R) % 16 == 0 ? std::max<int64_t>(16, R) : 16 * R;
+        for (int64_t rc = idx->s_pad - step; rc >= step; rc -= step) {
+            if (idx->s_pad % rc) continue;
+            const size_t le = WsLayout((int)idx->d, (int)idx->s, (int)idx->sub_d, (int)idx->p, esz, 1, 1, (int)K,
+                                       (int)idx->s_pad, (int)rc).lut_each;
+            const int g0 = (int)std::min<int64_t>(std::min<size_t>(WS_MAX_G, std::max<size_t>(1, lut_budget_bytes() / le)),
+                                                  std::max<int64_t>(1, P));
+            for (int g = g0; g >= min_g; --g)
+                for (int nb = WS_MAX_NBUF; nb >= min_nb; --nb)
+                    if (fits(g, nb, (int)rc) <= SMEM_LIMIT) {
+                        *plan = WsPlan{g, nb, fits(g, nb, (int)rc), gmem ? 1 : 0, (int)(idx->s_pad / rc), (int)rc};
+                        return true;
+                    }
         }
+        return false;
+    };
+    // Preference (measured on cfg2): >= 3 LUT slots (builders and scanners
+    // decoupled by a job of slack) with G >= 2; a table too large for that is
+    // row-chunked (cfg3 p8 f16 / f32: 120 / 240 KiB per list) before settling
+    // for fewer slots; a single slot (build, then scan) is the last resort
+    // before the per-query kernel.  Scan mode 2 prefers row chunks.
+    if (g_scan_mode.load() == 2 && chunked(3, 1)) return true;
+    if (unchunked(3, 2) || unchunked(3, 1) || chunked(3, 2) || chunked(3, 1) || unchunked(2, 1) || chunked(2, 1) ||
+        unchunked(1, 1))
+        return true;
     return false;
 }
 
@@ -671,14 +704,28 @@ int run_scan(ivfpq_index* idx, const float* d_q, int64_t nq, const uint64_t* d_p
         w.NBUF = plan.NBUF;
         w.gmem = plan.gmem;
         w.l2pf = (int64_t)idx->n_local * idx->s_pad > idx->l2_bytes ? 1 : 0;
+        w.nh = plan.nh;
+        w.rc = plan.nh > 1 ? plan.rc : 0;
+        w.rcc = (int)(plan.nh > 1 ? plan.rc / 16 : idx->s_pad / 16);
+        w.maxp = 0;
+        w.part = nullptr;
         CKR(idx->work.ensure(16));
         w.work = idx->work.as<int>();
         CK(cudaMemsetAsync(w.work, 0, sizeof(int), st));
         // plan: job descriptors + residual rows per query
         const WsLayout lay((int)idx->d, (int)idx->s, (int)idx->sub_d, (int)idx->p, lut_bytes_of(dt), plan.G, plan.NBUF,
-                           (int)K, (int)idx->s_pad);
+                           (int)K, (int)idx->s_pad, w.rc);
         const int d_pad = (int)lay.d_pad;
-        const int JMAX = (int)std::max<int64_t>(1, (P + plan.G - 1) / plan.G);
+        const int JMAX = (int)std::max<int64_t>(1, (P + plan.G - 1) / plan.G) * plan.nh;
+        const int grid = std::min<int64_t>(idx->num_sms, nq);
+        if (plan.nh > 1) {
+            // pairs one scanner warp owns in a job: ceil(ceil(blocks / 2) / SW),
+            // blocks <= G * ceil(longest list / 32)
+            const int64_t blocks = (int64_t)plan.G * ((idx->max_len + 31) / 32);
+            w.maxp = (int)std::max<int64_t>(1, ((blocks + 1) / 2 + WS_SW - 1) / WS_SW);
+            CKR(idx->part.ensure((size_t)grid * WS_SW * w.maxp * 64 * 4));
+            w.part = idx->part.as<float>();
+        }
         CKR(idx->plan_jobs.ensure((size_t)nq * JMAX * sizeof(WsJob)));
         CKR(idx->plan_rq.ensure((size_t)nq * JMAX * plan.G * d_pad * 4));
         CKR(idx->plan_nj.ensure((size_t)nq * 4));
@@ -688,11 +735,11 @@ int run_scan(ivfpq_index* idx, const float* d_q, int64_t nq, const uint64_t* d_p
         w.plan_njobs = idx->plan_nj.as<int>();
         w.plan_ncand = idx->plan_nc.as<long long>();
         w.JMAX = JMAX;
-        ws_plan_kernel<<<(unsigned)((nq + 7) / 8), 256, 0, st>>>(a, plan.G, d_pad, JMAX, idx->plan_jobs.as<WsJob>(),
+        ws_plan_kernel<<<(unsigned)((nq + 7) / 8), 256, 0, st>>>(a, plan.G, d_pad, JMAX, plan.nh,
+                                                                   idx->plan_jobs.as<WsJob>(),
                                                                    idx->plan_rq.as<float>(), idx->plan_nj.as<int>(),
                                                                    idx->plan_nc.as<long long>());
         KCHECK();
-        const int grid = std::min<int64_t>(idx->num_sms, nq);
         cudaError_t e = cudaErrorInvalidValue;
         switch (dt) {
             case LUT_F32: e = ws_launch_f32((int)idx->p, (int)idx->sub_d, w, plan.smem, grid, st); break;
@@ -749,7 +796,8 @@ int ivfpq_set_select_kernel(int mode) {
 }
 
 int ivfpq_set_scan_kernel(int mode) {
-    if (mode < 0 || mode > 1) return set_err(IVFPQ_EINVAL, "scan kernel mode must be 0 (auto) or 1 (v1)");
+    if (mode < 0 || mode > 2)
+        return set_err(IVFPQ_EINVAL, "scan kernel mode must be 0 (auto), 1 (v1) or 2 (prefer row-chunked LUT jobs)");
     g_scan_mode.store(mode);
     return IVFPQ_OK;
 }
@@ -853,6 +901,7 @@ int ivfpq_index_create(int device, const float* coarse, int64_t nlist, int64_t d
     idx->sub_d = sub_d;
     idx->s_pad = s_pad;
     idx->n_local = n_local;
+    for (int64_t i = 0; i < nl; ++i) idx->max_len = std::max<int64_t>(idx->max_len, off[i + 1] - off[i]);
     auto fail = [&](int rc) {
         ivfpq_index_destroy(idx);
         return rc;
@@ -921,7 +970,7 @@ int ivfpq_index_destroy(ivfpq_index* idx) {
                     idx->tc_img};
     for (void* ptr : ptrs)
         if (ptr) cudaFree(ptr);
-    for (DevBuf* b : {&idx->glut, &idx->q, &idx->dist, &idx->pkeys, &idx->oids, &idx->odist, &idx->oshort, &idx->keys, &idx->ncand,
+    for (DevBuf* b : {&idx->glut, &idx->part, &idx->q, &idx->dist, &idx->pkeys, &idx->oids, &idx->odist, &idx->oshort, &idx->keys, &idx->ncand,
                       &idx->work, &idx->plan_jobs, &idx->plan_rq, &idx->plan_nj, &idx->plan_nc, &idx->tc_sl,
                       &idx->flags})
         b->release();

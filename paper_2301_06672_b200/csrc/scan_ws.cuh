@@ -101,11 +101,18 @@ struct WsArgs {
     int NBUF;
     int gmem;              // 1: builders read the codebook from global memory (does not fit TMEM)
     int l2pf;              // 1: builders bulk-prefetch each job's codes into L2 (code store > L2)
+    // Row-chunked LUTs (tables larger than the shared-memory budget, e.g. the
+    // f32 LUT at s = 240, p = 8: 240 KiB): a group of G lists is processed as
+    // nh consecutive jobs, job h holding LUT rows [h*rc, (h+1)*rc) = code
+    // chunks [h*rcc, (h+1)*rcc); nh = 1 is the unchunked kernel.
+    int nh, rc, rcc;
+    int maxp;              // chunked: max pairs one scanner warp owns in a job
+    float* part;           // chunked: partial sums [grid][SW][maxp][64] carried between the chunks
     int* work;             // global query counter (zeroed before launch)
 };
 
 struct WsJob {
-    int qs, q, ng, last, nblk, pad;
+    int qs, q, ng, last, nblk, h;  // h: LUT row chunk of the job (0 unless chunked)
     int pref[WS_MAX_G + 1];
     int len[WS_MAX_G];
     int lc[WS_MAX_G];
@@ -337,17 +344,21 @@ __device__ __forceinline__ void tmem_st(uint32_t taddr, const uint32_t (&r)[X]) 
 // --------------------------------------------------------------- smem layout
 struct WsLayout {
     // lut rows are padded to R * jpt (jpt = ceil(s_pad / R)) so every builder
-    // thread runs the same number of rows; rq vectors likewise to R*jpt*sub_d.
+    // thread runs the same number of rows; rq vectors likewise to R*jpt*sub_d
+    // (row-chunked jobs: rc rows, a multiple of R and of 16, dividing s_pad).
     // Rows j >= s hold +0 entries (zero centers, zero residual), so the scan
     // reads whole 16-code chunks: the zero-code lookups past s add +0, which
     // leaves every sum bit-identical.
     size_t bars, qfree, tmem, cnt, jobs, pjobs, prepq, qst, lists, wbuf, prq, lut, total, lut_each, d_pad;
-    __host__ __device__ WsLayout(int d, int s, int sub_d, int logn, int esize, int G, int NBUF, int K, int s_pad) {
+    // rc: LUT rows held per job (row-chunked jobs), 0 = all R * jpt rows.
+    __host__ __device__ WsLayout(int d, int s, int sub_d, int logn, int esize, int G, int NBUF, int K, int s_pad,
+                                 int rc = 0) {
         const int N = 1 << logn, R = WS_R(N), jpt = (s_pad + R - 1) / R;
         (void)d;
         (void)s;
-        lut_each = (((size_t)R * jpt * N * esize) + 255) & ~(size_t)255;  // 256-aligned (PRMT addressing)
-        d_pad = (size_t)R * jpt * sub_d;
+        const int rows = rc > 0 ? rc : R * jpt;
+        lut_each = (((size_t)rows * N * esize) + 255) & ~(size_t)255;  // 256-aligned (PRMT addressing)
+        d_pad = (size_t)rows * sub_d;
         bars = 0;                                                         // pfull[PD], full[MAX_NBUF]
         qfree = (WS_PD + WS_MAX_NBUF) * 8;                                // query-state free barriers [NQS]
         tmem = qfree + WS_NQS * 8;                                        // u32: TMEM base address
@@ -464,8 +475,10 @@ struct WsBuild {
     // every list of the job.  The residual loads and table stores are plain
     // C++ shared-memory accesses (not volatile asm), so ptxas can interleave
     // the independent entry chains of the two rows and of consecutive lists.
+    // Rows i0 .. i0+jpt-1 of the thread's owned rows (a row chunk); rq and lut
+    // hold the chunk only (local row il = i - i0).
     __device__ __forceinline__ void build(const uint8_t* rq, uint32_t rq_stride, uint8_t* lut, uint32_t lut_stride,
-                                          int ng, int jpt) const {
+                                          int ng, int jpt, int i0) const {
         constexpr int E = sizeof(T);
         const uint8_t* rqb = rq + (size_t)jr * SUB_D * 4;
         uint8_t* lb = lut + ((size_t)jr * N + 4 * u) * E;
@@ -474,8 +487,8 @@ struct WsBuild {
 #pragma unroll 1
         for (; i + 2 <= jpt; i += 2) {
             uint32_t c0[CPI], c1[CPI];
-            row(i, c0);
-            row(i + 1, c1);
+            row(i0 + i, c0);
+            row(i0 + i + 1, c1);
             if constexpr (!GMEM) tmem_wait_ld();
             u64 cenA[2][SUB_D], cenB[2][SUB_D];
 #pragma unroll
@@ -511,7 +524,7 @@ struct WsBuild {
         }
         if (i < jpt) {
             uint32_t c[CPI];
-            row(i, c);
+            row(i0 + i, c);
             if constexpr (!GMEM) tmem_wait_ld();
             u64 cen[2][SUB_D];
 #pragma unroll
@@ -785,6 +798,7 @@ struct WsPair {
     const uint8_t* p0;
     const uint8_t* p1;
     uint32_t st0, st1;
+    int k, h;               // pair index in the job, the job's row chunk (chunked mode)
 };
 
 // A job's list table held lane-parallel (lane g < ng describes list g), read
@@ -794,10 +808,14 @@ struct WsJobTab {
     int len;        // its vector count
     int off;        // its first vector
     int nblk, qs;
-    __device__ __forceinline__ void load(const WsJob* J, int lane) {
+    int h;          // the job's LUT row chunk (chunked mode), else 0
+    int next;       // chunked mode: this warp's next pair index (static ownership)
+    __device__ __forceinline__ void load(const WsJob* J, int lane, int sw) {
         const int ng = J->ng;
         nblk = J->nblk;
         qs = J->qs;
+        h = J->h;
+        next = sw;
         pref = lane < ng ? J->pref[lane] : 0x7fffffff;
         len = lane < ng ? J->len[lane] : 0;
         off = lane < ng ? (int)J->off[lane] : 0;
@@ -815,16 +833,27 @@ struct WsJobTab {
     }
 };
 
-// Dynamic work distribution inside a job: lane 0 takes the next pair index
-// from the slot's counter (reset by the builders when they fill the slot), so
-// scanner warps finish a job within one pair of each other.
-__device__ __forceinline__ bool ws_grab(const WsJobTab& T, int* cnt, int slot, uint32_t slot_base, uint32_t lut_each,
-                                        const uint8_t* codes, int s_pad, int lane, WsPair& p) {
+// Work distribution inside a job.  Unchunked: lane 0 takes the next pair
+// index from the slot's counter (reset by the builders when they fill the
+// slot), so scanner warps finish a job within one pair of each other.
+// Chunked (CH): pair k is always scanned by warp k % SW, in every chunk job of
+// its group, so the partial sums it carries between chunks stay with the warp
+// (in its own scratch) and chunk h+1 of a pair never starts before chunk h.
+template <bool CH>
+__device__ __forceinline__ bool ws_grab(WsJobTab& T, int* cnt, int slot, uint32_t slot_base, uint32_t lut_each,
+                                        const uint8_t* codes, int s_pad, int rcc, int lane, WsPair& p) {
     int k = 0;
-    if (lane == 0) k = atomicAdd(cnt + slot, 1);
-    k = __shfl_sync(0xffffffffu, k, 0);
+    if constexpr (CH) {
+        k = T.next;
+        T.next += WS_SW;
+    } else {
+        if (lane == 0) k = atomicAdd(cnt + slot, 1);
+        k = __shfl_sync(0xffffffffu, k, 0);
+    }
     if (2 * k >= T.nblk) return false;
     p.qs = T.qs;
+    p.k = k;
+    p.h = T.h;
     int g;
     T.block(2 * k, g, p.nb0, p.vo0);
     p.base0 = slot_base + (uint32_t)g * lut_each;
@@ -838,10 +867,12 @@ __device__ __forceinline__ bool ws_grab(const WsJobTab& T, int* cnt, int slot, u
     }
     WS_CHECK(p.nb0 >= 1 && p.nb0 <= 32 && p.nb1 >= 0 && p.nb1 <= 32 && p.vo0 >= 0 && p.vo1 >= 0);
     const int l0 = min(lane, p.nb0 - 1), l1 = min(lane, max(p.nb1 - 1, 0));
-    p.p0 = codes + (long long)p.vo0 * s_pad + l0 * 16;
-    p.p1 = codes + (long long)p.vo1 * s_pad + l1 * 16;
     p.st0 = (uint32_t)p.nb0 * 16u;
     p.st1 = (uint32_t)p.nb1 * 16u;
+    // chunk 0 of the job's code range is chunk h*rcc of the vector (CH), else 0
+    const int c0 = CH ? T.h * rcc : 0;
+    p.p0 = codes + (long long)p.vo0 * s_pad + l0 * 16 + c0 * p.st0;
+    p.p1 = codes + (long long)p.vo1 * s_pad + l1 * 16 + c0 * p.st1;
     return true;
 }
 
@@ -945,14 +976,19 @@ __device__ __forceinline__ void ws_job_end(const ScanArgs& a, const WsJob* J, Ws
 // comes from the same job, else from the next job if its LUTs are already
 // built.  NCH > 0: the chunk count s_pad/16 as a compile-time constant (the
 // BASELINE shapes; straight-line code), 0: read from the arguments.
-template <int DT, int LOGN, int NCH>
-__device__ void ws_scanner(const ScanArgs& a, WsJob* jobs, int* cnt, u64* full, int NBUF, WsQuery* qst, u64* lists,
-                           int K, uint32_t lut_s0, uint32_t slot_bytes, uint32_t lut_each, WarpTopK& tk, u64* qfree,
-                           int lane) {
+template <int DT, int LOGN, int NCH, bool CH>
+__device__ void ws_scanner(const ScanArgs& a, const WsArgs& w, WsJob* jobs, int* cnt, u64* full, int NBUF,
+                           WsQuery* qst, u64* lists, int K, uint32_t lut_s0, uint32_t slot_bytes, uint32_t lut_each,
+                           WarpTopK& tk, u64* qfree, int sw, int lane) {
     constexpr int N = 1 << LOGN;
     constexpr int E = (int)sizeof(typename LutTraits<DT>::T);
     constexpr int NS = NCH == 0 || NCH >= 4 ? 4 : NCH;  // chunk registers per block
-    const int nch = NCH > 0 ? NCH : a.s_pad >> 4;      // LUT rows >= s are +0: whole chunks are exact
+    // code chunks (16 codes) per job: all of them (LUT rows >= s are +0, so
+    // whole chunks are exact), or a row chunk's rcc
+    const int nch = NCH > 0 ? NCH : w.rcc;
+    const int rcc = w.rcc, nh = w.nh;
+    // chunked: this warp's partial sums, 64 floats (32 lanes x 2 vectors) per owned pair
+    u64* part = CH ? reinterpret_cast<u64*>(w.part) + ((size_t)blockIdx.x * WS_SW + sw) * w.maxp * 32 + lane : nullptr;
     const int s_pad = a.s_pad;
     u64 pol;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
@@ -964,8 +1000,8 @@ __device__ void ws_scanner(const ScanArgs& a, WsJob* jobs, int* cnt, u64* full, 
     WsJobTab ct, nt;
     mbar_wait(full, 0);
     if (jobs[0].qs < 0) return;
-    ct.load(jobs, lane);
-    bool have = ws_grab(ct, cnt, 0, lut_s0, lut_each, codes, s_pad, lane, cur);
+    ct.load(jobs, lane, sw);
+    bool have = ws_grab<CH>(ct, cnt, 0, lut_s0, lut_each, codes, s_pad, rcc, lane, cur);
     auto load_first = [&](const WsPair& p) {
 #pragma unroll
         for (int u = 0; u < NS; ++u)
@@ -986,13 +1022,15 @@ __device__ void ws_scanner(const ScanArgs& a, WsJob* jobs, int* cnt, u64* full, 
             }
             mbar_wait(full + slot, ph);
             if (jobs[slot].qs < 0) break;
-            ct.load(jobs + slot, lane);
-            have = ws_grab(ct, cnt, slot, lut_s0 + (uint32_t)slot * slot_bytes, lut_each, codes, s_pad, lane, cur);
+            ct.load(jobs + slot, lane, sw);
+            have = ws_grab<CH>(ct, cnt, slot, lut_s0 + (uint32_t)slot * slot_bytes, lut_each, codes, s_pad, rcc, lane,
+                               cur);
             if (have) load_first(cur);
             continue;
         }
         // ---- the next pair: same job, else the next job if its LUTs are ready
-        bool hn = ws_grab(ct, cnt, slot, lut_s0 + (uint32_t)slot * slot_bytes, lut_each, codes, s_pad, lane, nxt);
+        bool hn = ws_grab<CH>(ct, cnt, slot, lut_s0 + (uint32_t)slot * slot_bytes, lut_each, codes, s_pad, rcc, lane,
+                              nxt);
         bool cross = false;
         if (!hn) {
             const int ns = slot + 1 == NBUF ? 0 : slot + 1;
@@ -1000,8 +1038,9 @@ __device__ void ws_scanner(const ScanArgs& a, WsJob* jobs, int* cnt, u64* full, 
             // (NBUF = 1: the "next" slot is this one; its previous phase would
             // test as complete, so there is no cross-job prefetch)
             if (NBUF > 1 && mbar_test(full + ns, (uint32_t)nph) && jobs[ns].qs >= 0) {
-                nt.load(jobs + ns, lane);
-                hn = ws_grab(nt, cnt, ns, lut_s0 + (uint32_t)ns * slot_bytes, lut_each, codes, s_pad, lane, nxt);
+                nt.load(jobs + ns, lane, sw);
+                hn = ws_grab<CH>(nt, cnt, ns, lut_s0 + (uint32_t)ns * slot_bytes, lut_each, codes, s_pad, rcc, lane,
+                                 nxt);
                 cross = true;  // (an empty next job is left to the blocking path)
             }
         }
@@ -1014,6 +1053,8 @@ __device__ void ws_scanner(const ScanArgs& a, WsJob* jobs, int* cnt, u64* full, 
         // ---- scan the current pair
         const uint32_t base0 = cur.base0, base1 = cur.base1;
         u64 acc = pk2(0.f, 0.f);
+        // chunked: continue the sums of this pair's earlier row chunks (sequential in j)
+        if (CH && cur.h > 0) acc = part[(size_t)((cur.k - sw) / WS_SW) * 32];
 #pragma unroll(NCH > 0 ? 1 : 1)
         for (int cg = 0; cg < nch; cg += 4) {
 #pragma unroll
@@ -1028,8 +1069,10 @@ __device__ void ws_scanner(const ScanArgs& a, WsJob* jobs, int* cnt, u64* full, 
                 }
             }
         }
-        // ---- offers against the query's shared threshold
-        {
+        // ---- offers against the query's shared threshold (chunked: after the last chunk)
+        if (CH && cur.h < nh - 1) {
+            part[(size_t)((cur.k - sw) / WS_SW) * 32] = acc;
+        } else {
             float r0, r1;
             upk2(acc, r0, r1);
             const int qs = cur.qs;
@@ -1066,7 +1109,7 @@ __device__ void ws_scanner(const ScanArgs& a, WsJob* jobs, int* cnt, u64* full, 
 // its G padded residual rows rq = fl(q - coarse[c]) to global memory, where
 // the search kernel's prep warp fetches them with two TMA bulk copies.
 // Also the query's job count and candidate count (all probes, owned or not).
-__global__ void __launch_bounds__(256) ws_plan_kernel(const ScanArgs a, int G, int d_pad, int JMAX, WsJob* jobs,
+__global__ void __launch_bounds__(256) ws_plan_kernel(const ScanArgs a, int G, int d_pad, int JMAX, int nh, WsJob* jobs,
                                                       float* rq, int* njobs, long long* ncand)
 #ifndef IVFPQ_DEFINE_PLAN_KERNEL
     ;  // defined in ivfpq_b200.cu
@@ -1085,31 +1128,41 @@ __global__ void __launch_bounds__(256) ws_plan_kernel(const ScanArgs a, int G, i
     const float* qv = a.queries + (size_t)q * a.d;
     int pend = 0, nj = 0;
     long long nc = 0;
+    // One group of ng lists = nh jobs (row chunks h = 0..nh-1; nh = 1 unless
+    // the LUT is row-chunked).  Job h's residual block holds the chunk's slice
+    // of every list's rq (d_pad floats each), so the prep's TMA copy stays one
+    // contiguous range.
     auto emit = [&](int from, int ng, bool last) {
-        WS_CHECK(nj < JMAX && ng <= G);
-        WsJob* J = jobs + (size_t)q * JMAX + nj;
-        if (lane == 0) {
-            int pref = 0;
-            for (int g = 0; g < ng; ++g) {
-                J->lc[g] = lcq[from + g];
-                J->len[g] = lenq[from + g];
-                J->off[g] = offq[from + g];
-                J->pref[g] = pref;
-                pref += (lenq[from + g] + 31) >> 5;
+        WS_CHECK(nj + nh <= JMAX && ng <= G);
+        for (int h = 0; h < nh; ++h) {
+            WsJob* J = jobs + (size_t)q * JMAX + nj + h;
+            if (lane == 0) {
+                int pref = 0;
+                for (int g = 0; g < ng; ++g) {
+                    J->lc[g] = lcq[from + g];
+                    J->len[g] = lenq[from + g];
+                    J->off[g] = offq[from + g];
+                    J->pref[g] = pref;
+                    pref += (lenq[from + g] + 31) >> 5;
+                }
+                J->pref[ng] = pref;
+                J->nblk = pref;
+                J->ng = ng;
+                J->q = q;
+                J->qs = 0;
+                J->h = h;
+                J->last = last && h == nh - 1 ? 1 : 0;
             }
-            J->pref[ng] = pref;
-            J->nblk = pref;
-            J->ng = ng;
-            J->q = q;
-            J->qs = 0;
-            J->last = last ? 1 : 0;
+            float* r = rq + ((size_t)q * JMAX + nj + h) * G * d_pad;
+            for (int g = 0; g < ng; ++g) {
+                const float* cv = a.coarse + (size_t)lcq[from + g] * a.d;
+                for (int x = lane; x < d_pad; x += 32) {
+                    const int t = h * d_pad + x;
+                    r[g * d_pad + x] = t < a.d ? __fsub_rn(qv[t], cv[t]) : 0.0f;
+                }
+            }
         }
-        float* r = rq + ((size_t)q * JMAX + nj) * G * d_pad;
-        for (int g = 0; g < ng; ++g) {
-            const float* cv = a.coarse + (size_t)lcq[from + g] * a.d;
-            for (int x = lane; x < d_pad; x += 32) r[g * d_pad + x] = x < a.d ? __fsub_rn(qv[x], cv[x]) : 0.0f;
-        }
-        ++nj;
+        nj += nh;
     };
     for (int base = 0; base < a.P; base += 32) {
         const int pi = base + lane;
@@ -1180,17 +1233,18 @@ __global__ void __launch_bounds__(256) ws_plan_kernel(const ScanArgs a, int G, i
 }
 #endif
 
-template <int DT, int LOGN, int SUB_D, bool GMEM, int NCH>
+template <int DT, int LOGN, int SUB_D, bool GMEM, int NCH, bool CH>
 __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) {
     using T = typename LutTraits<DT>::T;
     extern __shared__ __align__(1024) uint8_t ws_smem[];
     uint8_t* smem = ws_smem;
     const ScanArgs& a = w.a;
     const int G = a.G, NBUF = w.NBUF, K = a.K, NQS = WS_NQS;
-    const WsLayout L(a.d, a.s, SUB_D, LOGN, (int)sizeof(T), G, NBUF, K, a.s_pad);
+    const WsLayout L(a.d, a.s, SUB_D, LOGN, (int)sizeof(T), G, NBUF, K, a.s_pad, CH ? w.rc : 0);
     const size_t lut_each = L.lut_each;
-    const int d_pad = (int)L.d_pad;
-    const int jpt = (a.s_pad + WsBuild<DT, LOGN, SUB_D, GMEM>::R - 1) / WsBuild<DT, LOGN, SUB_D, GMEM>::R;  // rows per builder
+    const int d_pad = (int)L.d_pad;  // residual floats per list in a job (chunked: the chunk's rows)
+    constexpr int RB = WsBuild<DT, LOGN, SUB_D, GMEM>::R;
+    const int jpt = CH ? w.rc / RB : (a.s_pad + RB - 1) / RB;  // owned rows per builder thread per job
     u64* pfull = reinterpret_cast<u64*>(smem + L.bars);  // pfull[PD]: job + residuals prepared (TMA tx)
     u64* full = pfull + WS_PD;                            // full[NBUF]: LUTs ready
     WsJob* jobs = reinterpret_cast<WsJob*>(smem + L.jobs);
@@ -1317,7 +1371,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
 #endif
                 prefetch_l2(a.codes + PJ->off[t] * a.s_pad, (uint32_t)PJ->len[t] * (uint32_t)a.s_pad);
             B.build(reinterpret_cast<const uint8_t*>(prq) + (size_t)ps * G * d_pad * 4, (uint32_t)(d_pad * 4),
-                    lut_all + (size_t)slot * G * lut_each, (uint32_t)lut_each, PJ->ng, jpt);
+                    lut_all + (size_t)slot * G * lut_each, (uint32_t)lut_each, PJ->ng, jpt, CH ? PJ->h * jpt : 0);
             __syncwarp();  // the warp's LUT stores / prep reads are ordered before its arrivals
             if (lane == 0) mbar_arrive(full + slot);
             nbar_arrive(WS_BAR_PEMPTY0 + ps, WS_BAR_PEMPTY_N);
@@ -1338,9 +1392,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
         const int sw = warp - WS_BW;
         u64* wb = reinterpret_cast<u64*>(smem + L.wbuf) + (size_t)sw * 2 * WS_WBUF;
         WarpTopK tk{wb, wb + WS_WBUF, 0, K <= WS_PRIV_K ? lists + (size_t)sw * WS_NQS * K : nullptr};
-        ws_scanner<DT, LOGN, NCH>(a, jobs, reinterpret_cast<int*>(smem + L.cnt), full, NBUF, qst, lists, K,
-                                  smem_addr(lut_all), (uint32_t)(G * lut_each), (uint32_t)lut_each, tk,
-                                  reinterpret_cast<u64*>(smem + L.qfree), lane);
+        ws_scanner<DT, LOGN, NCH, CH>(a, w, jobs, reinterpret_cast<int*>(smem + L.cnt), full, NBUF, qst, lists, K,
+                                      smem_addr(lut_all), (uint32_t)(G * lut_each), (uint32_t)lut_each, tk,
+                                      reinterpret_cast<u64*>(smem + L.qfree), sw, lane);
     }
 }
 

@@ -9,12 +9,12 @@ namespace ivfpq {
 
 // The dynamic-smem attribute is per device context, so it is set before every
 // launch (cheap) instead of once per process.
-template <int DT, int LOGN, int SUB_D, bool GMEM, int NCH>
+template <int DT, int LOGN, int SUB_D, bool GMEM, int NCH, bool CH = false>
 cudaError_t ws_launch_k(const WsArgs& w, size_t smem, int grid, cudaStream_t st) {
-    cudaError_t e = cudaFuncSetAttribute(scan_ws_kernel<DT, LOGN, SUB_D, GMEM, NCH>,
+    cudaError_t e = cudaFuncSetAttribute(scan_ws_kernel<DT, LOGN, SUB_D, GMEM, NCH, CH>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    scan_ws_kernel<DT, LOGN, SUB_D, GMEM, NCH><<<grid, WS_THREADS, smem, st>>>(w);
+    scan_ws_kernel<DT, LOGN, SUB_D, GMEM, NCH, CH><<<grid, WS_THREADS, smem, st>>>(w);
     return cudaGetLastError();
 }
 
@@ -24,6 +24,12 @@ cudaError_t ws_launch_k(const WsArgs& w, size_t smem, int grid, cudaStream_t st)
 //   cfg3 s=240 (sub_d=4): p=8 with the codebook in global memory, p=5 in TMEM.
 template <int DT, int LOGN, int SUB_D, bool GMEM>
 cudaError_t ws_launch_g(const WsArgs& w, size_t smem, int grid, cudaStream_t st) {
+    // row-chunked LUT jobs (tables beyond the shared-memory budget, only with
+    // 2^p >= 32 codes): runtime chunk count per job
+    if (w.nh > 1) {
+        if constexpr (LOGN >= 5) return ws_launch_k<DT, LOGN, SUB_D, GMEM, 0, true>(w, smem, grid, st);
+        return cudaErrorNotSupported;
+    }
     const int nch = w.a.s_pad >> 4;
     if constexpr (LOGN == 8 && SUB_D == 2 && !GMEM) {
         if (nch == 4) return ws_launch_k<DT, LOGN, SUB_D, GMEM, 4>(w, smem, grid, st);

@@ -23,12 +23,14 @@ def pkg():
     return p
 
 
-@pytest.fixture(params=["auto", "v1"])
+@pytest.fixture(params=["auto", "v1", "chunked"])
 def scan_kernel(request, pkg):
-    """Run a test with the persistent warp-specialised scan (auto) and with the
-    per-query scan kernel (v1)."""
+    """Run a test with the persistent warp-specialised scan (auto), with the
+    per-query scan kernel (v1), and with the persistent kernel preferring
+    row-chunked LUT jobs (partial sums carried between chunks) wherever the
+    shape allows them."""
     from paper_2301_06672_b200 import _lib
-    _lib.check(_lib.lib.ivfpq_set_scan_kernel(0 if request.param == "auto" else 1))
+    _lib.check(_lib.lib.ivfpq_set_scan_kernel({"auto": 0, "v1": 1, "chunked": 2}[request.param]))
     yield request.param
     _lib.check(_lib.lib.ivfpq_set_scan_kernel(0))
 
