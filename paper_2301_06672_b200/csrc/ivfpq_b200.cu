@@ -633,16 +633,15 @@ bool ws_plan(const ivfpq_index* idx, int64_t P, int64_t K, int dt, WsPlan* plan)
         }
         return false;
     };
-    // Preference (measured on cfg2): >= 3 LUT slots (builders and scanners
-    // decoupled by a job of slack) with G >= 2; a table too large for that is
-    // row-chunked (cfg3 p8 f16 / f32: 120 / 240 KiB per list) before settling
-    // for fewer slots; a single slot (build, then scan) is the last resort
-    // before the per-query kernel.  Scan mode 2 prefers row chunks.
+    // Preference (measured): >= 3 LUT slots (builders and scanners decoupled by
+    // a job of slack) with G >= 2 (cfg2), then fewer slots down to one (cfg3 p8
+    // f16, 120 KiB: one slot 107 ms vs row chunks 127 ms); a table larger than
+    // shared memory is row-chunked, the largest chunk first (cfg3 p8 f32:
+    // 48-row chunks 145 ms, 16-row chunks x 4 lists 178 ms, the per-query
+    // kernel with a global-memory table ~275 ms).  Scan mode 2 prefers chunks.
     if (g_scan_mode.load() == 2 && chunked(3, 1)) return true;
-    if (unchunked(3, 2) || unchunked(3, 1) || chunked(3, 2) || chunked(3, 1) || unchunked(2, 1) || chunked(2, 1) ||
-        unchunked(1, 1))
-        return true;
-    return false;
+    return unchunked(3, 2) || unchunked(3, 1) || unchunked(2, 1) || unchunked(1, 1) || chunked(3, 1) || chunked(2, 1) ||
+           chunked(1, 1);
 }
 
 int run_scan(ivfpq_index* idx, const float* d_q, int64_t nq, const uint64_t* d_pk, int64_t P, int64_t K, int dt,

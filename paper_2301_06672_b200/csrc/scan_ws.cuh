@@ -1367,7 +1367,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
 #ifdef WS_NO_L2PF  // (variant switch for experiments)
             if (false)
 #else
-            if (w.l2pf && t < PJ->ng)
+            if (w.l2pf && PJ->h == 0 && t < PJ->ng)
 #endif
                 prefetch_l2(a.codes + PJ->off[t] * a.s_pad, (uint32_t)PJ->len[t] * (uint32_t)a.s_pad);
             B.build(reinterpret_cast<const uint8_t*>(prq) + (size_t)ps * G * d_pad * 4, (uint32_t)(d_pad * 4),
