@@ -45,9 +45,11 @@ int ivfpq_version(void);
 int ivfpq_device_count(int *n);
 /* Upper bound on k and nprobe supported by the device top-k. */
 int ivfpq_max_k(void);
-/* Scan kernel selection (testing): 0 = auto (persistent warp-specialised
- * kernel when the shape fits, else the per-query kernel), 1 = force the
- * per-query kernel. */
+/* Scan kernel selection (testing; every mode is exact): 0 = auto (persistent
+ * warp-specialised kernel when the shape fits -- warp layout B, 4 builder + 15
+ * scanner warps, for scan-heavy shapes, else layout A, 8 + 11 -- otherwise the
+ * per-query kernel), 1 = force the per-query kernel, 2 = prefer row-chunked
+ * LUT jobs, 3 = layout A only, 4 = layout B wherever it is built. */
 int ivfpq_set_scan_kernel(int mode);
 /* Coarse-select (K1) kernel selection (testing): 0 = auto (tensor-core TF32
  * nomination + exact re-rank when the shape fits), 1 = exact SIMT kernel only,

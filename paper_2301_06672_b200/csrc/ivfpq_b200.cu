@@ -579,15 +579,16 @@ bool ws_disabled() {
 
 // Can the v2 kernel run this shape?  Builder registers: ceil(s / R) subspaces
 // of a 4-code quad, R = 1024 / 2^p row groups, at most 32 / sub_d of them.
+template <class C>
 bool ws_plan(const ivfpq_index* idx, int64_t P, int64_t K, int dt, WsPlan* plan) {
     if (ws_disabled() || idx->num_sms <= 0) return false;
     const int64_t N = 1LL << idx->p;
     if (idx->p < 2 || idx->sub_d < 1 || idx->sub_d > 4 || K > WS_MAX_K) return false;
-    const int64_t R = WS_R((int)N);
-    const int64_t jpt = WS_JPT((int)idx->sub_d);
+    const int64_t R = C::R((int)N);
+    const int64_t jpt = C::JPT((int)idx->sub_d);
     // rows per builder thread beyond the TMEM budget: codebook read from global
     const bool gmem = (idx->s_pad + R - 1) / R > jpt;
-    const size_t lut_each = WsLayout((int)idx->d, (int)idx->s, (int)idx->sub_d, (int)idx->p, lut_bytes_of((int)dt), 1,
+    const size_t lut_each = WsLayout<C>((int)idx->d, (int)idx->s, (int)idx->sub_d, (int)idx->p, lut_bytes_of((int)dt), 1,
                                      2, (int)K, (int)idx->s_pad).lut_each;
     int G = (int)std::max<size_t>(1, std::min<size_t>(WS_MAX_G, lut_budget_bytes() / lut_each));
     G = (int)std::min<int64_t>(G, std::max<int64_t>(1, P));
@@ -598,7 +599,7 @@ bool ws_plan(const ivfpq_index* idx, int64_t P, int64_t K, int dt, WsPlan* plan)
     const int G0 = G;
     const int esz = lut_bytes_of((int)dt);
     auto fits = [&](int g, int nb, int rc) {
-        return WsLayout((int)idx->d, (int)idx->s, (int)idx->sub_d, (int)idx->p, esz, g, nb, (int)K, (int)idx->s_pad, rc)
+        return WsLayout<C>((int)idx->d, (int)idx->s, (int)idx->sub_d, (int)idx->p, esz, g, nb, (int)K, (int)idx->s_pad, rc)
             .total;
     };
     // unchunked: the largest G with >= min_nb LUT slots
@@ -620,7 +621,7 @@ bool ws_plan(const ivfpq_index* idx, int64_t P, int64_t K, int dt, WsPlan* plan)
         const int64_t step = std::max<int64_t>(16, R) % 16 == 0 ? std::max<int64_t>(16, R) : 16 * R;
         for (int64_t rc = idx->s_pad - step; rc >= step; rc -= step) {
             if (idx->s_pad % rc) continue;
-            const size_t le = WsLayout((int)idx->d, (int)idx->s, (int)idx->sub_d, (int)idx->p, esz, 1, 1, (int)K,
+            const size_t le = WsLayout<C>((int)idx->d, (int)idx->s, (int)idx->sub_d, (int)idx->p, esz, 1, 1, (int)K,
                                        (int)idx->s_pad, (int)rc).lut_each;
             const int g0 = (int)std::min<int64_t>(std::min<size_t>(WS_MAX_G, std::max<size_t>(1, lut_budget_bytes() / le)),
                                                   std::max<int64_t>(1, P));
@@ -642,6 +643,83 @@ bool ws_plan(const ivfpq_index* idx, int64_t P, int64_t K, int dt, WsPlan* plan)
     if (g_scan_mode.load() == 2 && chunked(3, 1)) return true;
     return unchunked(3, 2) || unchunked(3, 1) || unchunked(2, 1) || unchunked(1, 1) || chunked(3, 1) || chunked(2, 1) ||
            chunked(1, 1);
+}
+
+// Shapes the layout-B kernels are built for (ws_launch.cuh): cfg4 (p 8, sub_d 2,
+// s 48), cfg5 (p 8, sub_d 3, s 32), cfg3 p5 (p 5, sub_d 4, s 240), codebook in TMEM.
+bool ws_layout_b_supported(const ivfpq_index* idx) {
+    const int64_t nch = idx->s_pad / 16;
+    if (idx->s_pad > WsCfgB::R((int)(1 << idx->p)) * WsCfgB::JPT((int)idx->sub_d)) return false;  // not TMEM
+    return (idx->p == 8 && idx->sub_d == 2 && nch == 3) || (idx->p == 8 && idx->sub_d == 3 && nch == 2) ||
+           (idx->p == 5 && idx->sub_d == 4 && nch == 15);
+}
+
+// Plan + launch of the persistent scan kernel with warp layout C; *done =
+// false when the shape cannot be planned or the build has no kernel for it.
+template <class C>
+int run_scan_ws(ivfpq_index* idx, ScanArgs a, int64_t nq, int64_t P, int64_t K, int dt, cudaStream_t st, int layout,
+                bool* done) {
+    *done = false;
+    WsPlan plan;
+    if (!ws_plan<C>(idx, P, K, dt, &plan)) return IVFPQ_OK;
+    if (layout == 1 && plan.nh > 1) return IVFPQ_OK;
+    a.G = plan.G;
+    WsArgs w;
+    w.a = a;
+    w.NBUF = plan.NBUF;
+    w.gmem = plan.gmem;
+    w.l2pf = (int64_t)idx->n_local * idx->s_pad > idx->l2_bytes ? 1 : 0;
+    w.nh = plan.nh;
+    w.rc = plan.nh > 1 ? plan.rc : 0;
+    w.rcc = (int)(plan.nh > 1 ? plan.rc / 16 : idx->s_pad / 16);
+    w.maxp = 0;
+    w.part = nullptr;
+    CKR(idx->work.ensure(16));
+    w.work = idx->work.as<int>();
+    CK(cudaMemsetAsync(w.work, 0, sizeof(int), st));
+    // plan: job descriptors + residual rows per query
+    const WsLayout<C> lay((int)idx->d, (int)idx->s, (int)idx->sub_d, (int)idx->p, lut_bytes_of(dt), plan.G, plan.NBUF,
+                       (int)K, (int)idx->s_pad, w.rc);
+    const int d_pad = (int)lay.d_pad;
+    const int JMAX = (int)std::max<int64_t>(1, (P + plan.G - 1) / plan.G) * plan.nh;
+    const int grid = std::min<int64_t>(idx->num_sms, nq);
+    if (plan.nh > 1) {
+        // pairs one scanner warp owns in a job: ceil(ceil(blocks / 2) / SW),
+        // blocks <= G * ceil(longest list / 32)
+        const int64_t blocks = (int64_t)plan.G * ((idx->max_len + 31) / 32);
+        w.maxp = (int)std::max<int64_t>(1, ((blocks + 1) / 2 + C::SW - 1) / C::SW);
+        CKR(idx->part.ensure((size_t)grid * C::SW * w.maxp * 64 * 4));
+        w.part = idx->part.as<float>();
+    }
+    CKR(idx->plan_jobs.ensure((size_t)nq * JMAX * sizeof(WsJob)));
+    CKR(idx->plan_rq.ensure((size_t)nq * JMAX * plan.G * d_pad * 4));
+    CKR(idx->plan_nj.ensure((size_t)nq * 4));
+    CKR(idx->plan_nc.ensure((size_t)nq * 8));
+    w.plan_jobs = idx->plan_jobs.as<WsJob>();
+    w.plan_rq = idx->plan_rq.as<float>();
+    w.plan_njobs = idx->plan_nj.as<int>();
+    w.plan_ncand = idx->plan_nc.as<long long>();
+    w.JMAX = JMAX;
+    ws_plan_kernel<<<(unsigned)((nq + 7) / 8), 256, 0, st>>>(a, plan.G, d_pad, JMAX, plan.nh,
+                                                               idx->plan_jobs.as<WsJob>(),
+                                                               idx->plan_rq.as<float>(), idx->plan_nj.as<int>(),
+                                                               idx->plan_nc.as<long long>());
+    KCHECK();
+    cudaError_t e = cudaErrorInvalidValue;
+    switch (dt) {
+        case LUT_F32: e = ws_launch_f32(layout, (int)idx->p, (int)idx->sub_d, w, plan.smem, grid, st); break;
+        case LUT_F16: e = ws_launch_f16(layout, (int)idx->p, (int)idx->sub_d, w, plan.smem, grid, st); break;
+        case LUT_E5M3: e = ws_launch_e5m3(layout, (int)idx->p, (int)idx->sub_d, w, plan.smem, grid, st); break;
+        case LUT_E4M4: e = ws_launch_e4m4(layout, (int)idx->p, (int)idx->sub_d, w, plan.smem, grid, st); break;
+    }
+    if (e == cudaSuccess) {
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        *done = true;
+        return IVFPQ_OK;
+    }
+    if (e != cudaErrorNotSupported)
+        return set_err(IVFPQ_ECUDA, "scan_ws launch failed: %s", cudaGetErrorString(e));
+    return IVFPQ_OK;  // no kernel for this shape in this build: the caller falls back
 }
 
 int run_scan(ivfpq_index* idx, const float* d_q, int64_t nq, const uint64_t* d_pk, int64_t P, int64_t K, int dt,
@@ -694,65 +772,21 @@ int run_scan(ivfpq_index* idx, const float* d_q, int64_t nq, const uint64_t* d_p
     a.out_short = out_short;
     if (nq == 0) return IVFPQ_OK;
     // v2 (persistent, warp-specialised, codebook in tensor memory) when the
-    // shape fits its register/smem budget; v1 otherwise.
-    WsPlan plan;
-    if (ws_plan(idx, P, K, dt, &plan)) {
-        a.G = plan.G;
-        WsArgs w;
-        w.a = a;
-        w.NBUF = plan.NBUF;
-        w.gmem = plan.gmem;
-        w.l2pf = (int64_t)idx->n_local * idx->s_pad > idx->l2_bytes ? 1 : 0;
-        w.nh = plan.nh;
-        w.rc = plan.nh > 1 ? plan.rc : 0;
-        w.rcc = (int)(plan.nh > 1 ? plan.rc / 16 : idx->s_pad / 16);
-        w.maxp = 0;
-        w.part = nullptr;
-        CKR(idx->work.ensure(16));
-        w.work = idx->work.as<int>();
-        CK(cudaMemsetAsync(w.work, 0, sizeof(int), st));
-        // plan: job descriptors + residual rows per query
-        const WsLayout lay((int)idx->d, (int)idx->s, (int)idx->sub_d, (int)idx->p, lut_bytes_of(dt), plan.G, plan.NBUF,
-                           (int)K, (int)idx->s_pad, w.rc);
-        const int d_pad = (int)lay.d_pad;
-        const int JMAX = (int)std::max<int64_t>(1, (P + plan.G - 1) / plan.G) * plan.nh;
-        const int grid = std::min<int64_t>(idx->num_sms, nq);
-        if (plan.nh > 1) {
-            // pairs one scanner warp owns in a job: ceil(ceil(blocks / 2) / SW),
-            // blocks <= G * ceil(longest list / 32)
-            const int64_t blocks = (int64_t)plan.G * ((idx->max_len + 31) / 32);
-            w.maxp = (int)std::max<int64_t>(1, ((blocks + 1) / 2 + WS_SW - 1) / WS_SW);
-            CKR(idx->part.ensure((size_t)grid * WS_SW * w.maxp * 64 * 4));
-            w.part = idx->part.as<float>();
-        }
-        CKR(idx->plan_jobs.ensure((size_t)nq * JMAX * sizeof(WsJob)));
-        CKR(idx->plan_rq.ensure((size_t)nq * JMAX * plan.G * d_pad * 4));
-        CKR(idx->plan_nj.ensure((size_t)nq * 4));
-        CKR(idx->plan_nc.ensure((size_t)nq * 8));
-        w.plan_jobs = idx->plan_jobs.as<WsJob>();
-        w.plan_rq = idx->plan_rq.as<float>();
-        w.plan_njobs = idx->plan_nj.as<int>();
-        w.plan_ncand = idx->plan_nc.as<long long>();
-        w.JMAX = JMAX;
-        ws_plan_kernel<<<(unsigned)((nq + 7) / 8), 256, 0, st>>>(a, plan.G, d_pad, JMAX, plan.nh,
-                                                                   idx->plan_jobs.as<WsJob>(),
-                                                                   idx->plan_rq.as<float>(), idx->plan_nj.as<int>(),
-                                                                   idx->plan_nc.as<long long>());
-        KCHECK();
-        cudaError_t e = cudaErrorInvalidValue;
-        switch (dt) {
-            case LUT_F32: e = ws_launch_f32((int)idx->p, (int)idx->sub_d, w, plan.smem, grid, st); break;
-            case LUT_F16: e = ws_launch_f16((int)idx->p, (int)idx->sub_d, w, plan.smem, grid, st); break;
-            case LUT_E5M3: e = ws_launch_e5m3((int)idx->p, (int)idx->sub_d, w, plan.smem, grid, st); break;
-            case LUT_E4M4: e = ws_launch_e4m4((int)idx->p, (int)idx->sub_d, w, plan.smem, grid, st); break;
-        }
-        if (e == cudaSuccess) {
-            g_launches.fetch_add(1, std::memory_order_relaxed);
-            return IVFPQ_OK;
-        }
-        if (e != cudaErrorNotSupported)
-            return set_err(IVFPQ_ECUDA, "scan_ws launch failed: %s", cudaGetErrorString(e));
-        a.G = G;  // register budget not met by this build: per-query kernel
+    // shape fits its register/smem budget; v1 otherwise.  Layout B (4 builder +
+    // 15 scanner warps) for scan-heavy shapes (>= 2 lookups per LUT entry on
+    // average: cfg4, cfg5, cfg3 p5), layout A (8 + 11) otherwise.
+    const int mode = g_scan_mode.load();
+    const double per_entry = (double)idx->n_local / (double)std::max<int64_t>(1, idx->nlist_local) / (double)(1 << idx->p);
+    const bool want_b = mode == 4 || (mode == 0 && per_entry >= 2.0);
+    if (want_b && ws_layout_b_supported(idx)) {
+        bool done = false;
+        CKR(run_scan_ws<WsCfgB>(idx, a, nq, P, K, dt, st, 1, &done));
+        if (done) return IVFPQ_OK;
+    }
+    {
+        bool done = false;
+        CKR(run_scan_ws<WsCfgA>(idx, a, nq, P, K, dt, st, 0, &done));
+        if (done) return IVFPQ_OK;
     }
     return DISPATCH_DT_LOGN(dt, (int)idx->p, launch_scan_dt, a, smem, glut_p, grid, st);
 }
@@ -795,8 +829,10 @@ int ivfpq_set_select_kernel(int mode) {
 }
 
 int ivfpq_set_scan_kernel(int mode) {
-    if (mode < 0 || mode > 2)
-        return set_err(IVFPQ_EINVAL, "scan kernel mode must be 0 (auto), 1 (v1) or 2 (prefer row-chunked LUT jobs)");
+    if (mode < 0 || mode > 4)
+        return set_err(IVFPQ_EINVAL,
+                       "scan kernel mode must be 0 (auto), 1 (v1), 2 (prefer row-chunked LUT jobs), 3 (warp layout A "
+                       "only) or 4 (warp layout B where built)");
     g_scan_mode.store(mode);
     return IVFPQ_OK;
 }

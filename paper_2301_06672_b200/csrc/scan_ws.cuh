@@ -54,19 +54,29 @@ namespace ivfpq {
     } while (0)
 #endif
 
-#ifndef WS_BW_CFG
-#define WS_BW_CFG 8
-#define WS_SW_CFG 11
-#endif
-constexpr int WS_BW = WS_BW_CFG;             // builder warps (WS_BW/4 TMEM column groups)
-constexpr int WS_SW = WS_SW_CFG;             // scanner warps
-constexpr int WS_NB = WS_BW * 32;            // 512 builder threads
-constexpr int WS_PREP_WARP = WS_BW + WS_SW;   // warp 31: job preparation
-// Builder row geometry (shared by host plan and device): a builder thread owns
-// a quad of codes and ceil(s / WS_R(N)) subspace rows, at most WS_JPT(sub_d).
-__host__ __device__ constexpr int WS_R(int N) { return WS_NB * 4 / N; }
-__host__ __device__ constexpr int WS_JPT(int sub_d) { return 64 / (sub_d * WS_BW / 4); }
-constexpr int WS_THREADS = (WS_BW + WS_SW + 1) * 32;
+// Warp layout of the CTA: BW builder warps (a multiple of 4: TMEM lane
+// quarters), SW scanner warps, one prep warp.  Two layouts are built:
+//  * WsCfgA = 8 + 11: LUT-build-heavy shapes (cfg2: ~1.7 lookups per entry);
+//  * WsCfgB = 4 + 15: scan-heavy shapes (cfg5: 8 KiB LUTs and ~10-20 lookups
+//    per entry; the 8 builder warps of layout A idle ~40% of the time there
+//    while the scanners wait on the code stream).
+template <int BW_, int SW_>
+struct WsCfg {
+    static constexpr int BW = BW_;                     // builder warps
+    static constexpr int SW = SW_;                     // scanner warps
+    static constexpr int NB = BW * 32;                 // builder threads
+    static constexpr int PREP = BW + SW;               // the prep warp
+    static constexpr int THREADS = (BW + SW + 1) * 32;
+    static constexpr int BAR_EMPTY_N = NB + SW * 32;   // participants of a slot-free barrier
+    static constexpr int BAR_PEMPTY_N = NB + 32;       // participants of a ring-entry barrier
+    // Builder row geometry (shared by host plan and device): a builder thread
+    // owns a quad of codes and ceil(s / R(N)) subspace rows, at most JPT(sub_d).
+    __host__ __device__ static constexpr int R(int N) { return NB * 4 / N; }
+    __host__ __device__ static constexpr int JPT(int sub_d) { return 64 / (sub_d * BW / 4); }
+    static_assert(BW % 4 == 0, "builder warps fill TMEM lane quarters");
+};
+using WsCfgA = WsCfg<8, 11>;
+using WsCfgB = WsCfg<4, 15>;
 
 constexpr int WS_MAX_G = 8;
 constexpr int WS_MAX_NBUF = 6;
@@ -86,8 +96,6 @@ constexpr int WS_BAR_BUILD = 1;              // builders only (teardown)
 constexpr int WS_BAR_EMPTY0 = 2;             // + slot: LUT slot free   (builders sync, scanners arrive)
 constexpr int WS_BAR_PEMPTY0 = WS_BAR_EMPTY0 + WS_MAX_NBUF;  // + ring entry: prep entry consumed
 static_assert(WS_BAR_PEMPTY0 + WS_PD <= 16, "named barrier ids");
-constexpr int WS_BAR_EMPTY_N = WS_NB + WS_SW * 32;   // participants of a slot-free barrier
-constexpr int WS_BAR_PEMPTY_N = WS_NB + 32;          // participants of a ring-entry barrier
 
 
 struct WsJob;
@@ -260,7 +268,8 @@ __device__ __forceinline__ uint4 lds128(uint32_t a) {
     asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(a));
     return r;
 }
-__device__ __forceinline__ void bar_builders() { asm volatile("bar.sync %0, %1;" ::"n"(WS_BAR_BUILD), "n"(WS_NB) : "memory"); }
+template <int NB>
+__device__ __forceinline__ void bar_builders() { asm volatile("bar.sync %0, %1;" ::"n"(WS_BAR_BUILD), "n"(NB) : "memory"); }
 // Named-barrier hand-off: the consumer of a free slot waits with bar.sync (the
 // warp is descheduled, no polling), the releasing role signals with bar.arrive.
 __device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
@@ -342,6 +351,7 @@ __device__ __forceinline__ void tmem_st(uint32_t taddr, const uint32_t (&r)[X]) 
 }
 
 // --------------------------------------------------------------- smem layout
+template <class C>
 struct WsLayout {
     // lut rows are padded to R * jpt (jpt = ceil(s_pad / R)) so every builder
     // thread runs the same number of rows; rq vectors likewise to R*jpt*sub_d
@@ -353,7 +363,7 @@ struct WsLayout {
     // rc: LUT rows held per job (row-chunked jobs), 0 = all R * jpt rows.
     __host__ __device__ WsLayout(int d, int s, int sub_d, int logn, int esize, int G, int NBUF, int K, int s_pad,
                                  int rc = 0) {
-        const int N = 1 << logn, R = WS_R(N), jpt = (s_pad + R - 1) / R;
+        const int N = 1 << logn, R = C::R(N), jpt = (s_pad + R - 1) / R;
         (void)d;
         (void)s;
         const int rows = rc > 0 ? rc : R * jpt;
@@ -371,9 +381,9 @@ struct WsLayout {
         qst = (qst + 15) & ~(size_t)15;
         lists = qst + WS_NQS * sizeof(WsQuery);                           // top-k lists (WarpTopK):
         lists = (lists + 15) & ~(size_t)15;                               //  u64[SW][NQS][K] (K <= WS_PRIV_K)
-        wbuf = lists + (size_t)(K <= WS_PRIV_K ? WS_SW * WS_NQS * K : WS_NQS * 2 * K) * 8;  // or u64[NQS][2][K]
+        wbuf = lists + (size_t)(K <= WS_PRIV_K ? C::SW * WS_NQS * K : WS_NQS * 2 * K) * 8;  // or u64[NQS][2][K]
         //                                                                   u64[SW][2][WBUF]
-        prq = wbuf + (size_t)WS_SW * 2 * WS_WBUF * 8;                     // f32[PD][G][d_pad] (TMA-filled)
+        prq = wbuf + (size_t)C::SW * 2 * WS_WBUF * 8;                     // f32[PD][G][d_pad] (TMA-filled)
         prq = (prq + 127) & ~(size_t)127;
         lut = prq + (size_t)WS_PD * G * d_pad * 4;                        // [NBUF][G][lut_each]
         lut = (lut + 255) & ~(size_t)255;
@@ -386,15 +396,15 @@ struct WsLayout {
 // j = jr + R*i (jr = t / (N/4), R = 1024/N), i < jpt.  Its centers live in
 // TMEM: for owned row i, CPI columns hold c[m0..m0+3][0..SUB_D) (pairs packed
 // as (c[m0][x], c[m0+1][x]), (c[m0+2][x], c[m0+3][x])).
-template <int DT, int LOGN, int SUB_D, bool GMEM>
+template <class C, int DT, int LOGN, int SUB_D, bool GMEM>
 struct WsBuild {
     static constexpr int N = 1 << LOGN;
     static constexpr int NQ4 = N / 4;                                   // quads per subspace row
-    static constexpr int R = WS_R(N);                                   // row groups
-    static constexpr int JPT = WS_JPT(SUB_D);                           // max owned rows (host-checked)
+    static constexpr int R = C::R(N);                                   // row groups
+    static constexpr int JPT = C::JPT(SUB_D);                           // max owned rows (host-checked)
     static constexpr int CPI = SUB_D == 1 ? 4 : SUB_D == 2 ? 8 : 16;    // TMEM columns per owned row
     static constexpr int HALF = JPT * CPI;                              // columns per builder column group
-    static constexpr int NGRP = WS_BW / 4;                              // warps sharing a TMEM lane quarter
+    static constexpr int NGRP = C::BW / 4;                              // warps sharing a TMEM lane quarter
     static constexpr int NCOL = NGRP * HALF <= 256 ? 256 : 512;         // TMEM allocation
     static_assert(NGRP * HALF <= 512, "codebook does not fit TMEM");
     using T = typename LutTraits<DT>::T;
@@ -852,13 +862,13 @@ struct WsJobTab {
 // Chunked (CH): pair k is always scanned by warp k % SW, in every chunk job of
 // its group, so the partial sums it carries between chunks stay with the warp
 // (in its own scratch) and chunk h+1 of a pair never starts before chunk h.
-template <bool CH>
+template <class C, bool CH>
 __device__ __forceinline__ bool ws_grab(WsJobTab& T, int* cnt, int slot, uint32_t slot_base, uint32_t lut_each,
                                         const uint8_t* codes, int s_pad, int rcc, int lane, WsPair& p) {
     int k = 0;
     if constexpr (CH) {
         k = T.next;
-        T.next += WS_SW;
+        T.next += C::SW;
     } else {
         if (lane == 0) k = atomicAdd(cnt + slot, 1);
         k = __shfl_sync(0xffffffffu, k, 0);
@@ -900,6 +910,7 @@ __device__ __forceinline__ uint4 ws_ld(const uint8_t* p, u64 pol) {
 // End of this warp's part of the job in `slot`: at the query's last job, merge
 // the warp's candidates and let the last warp write the results and free the
 // query state; then release the LUT slot (named barrier, see the header).
+template <class C>
 __device__ __forceinline__ void ws_job_end(const ScanArgs& a, const WsJob* J, WsQuery* qst, u64* lists, int K,
                                            WarpTopK& tk, u64* qfree, int slot, int lane) {
     if (J->last) {
@@ -913,8 +924,8 @@ __device__ __forceinline__ void ws_job_end(const ScanArgs& a, const WsJob* J, Ws
             d = atomicAdd(&S->done, 1);
         }
         d = __shfl_sync(0xffffffffu, d, 0);
-        WS_CHECK(d >= 0 && d < WS_SW);
-        if (d == WS_SW - 1) {
+        WS_CHECK(d >= 0 && d < C::SW);
+        if (d == C::SW - 1) {
             __threadfence_block();
             const u64* r;
             if (tk.priv) {
@@ -922,7 +933,7 @@ __device__ __forceinline__ void ws_job_end(const ScanArgs& a, const WsJob* J, Ws
                 const size_t wstride = (size_t)WS_NQS * K;
                 const u64* L0 = lists + (size_t)qs * K;
                 for (int i = lane; i < K; i += 32) tk.buf[i] = L0[i];
-                for (int w = 1; w < WS_SW; ++w) {
+                for (int w = 1; w < C::SW; ++w) {
                     const u64* Lw = L0 + w * wstride;
                     __syncwarp();
                     for (int i = lane; i < K; i += 32) {
@@ -961,7 +972,7 @@ __device__ __forceinline__ void ws_job_end(const ScanArgs& a, const WsJob* J, Ws
             }
             __syncwarp();
             if (tk.priv) {
-                for (int i = lane; i < WS_SW * K; i += 32)
+                for (int i = lane; i < C::SW * K; i += 32)
                     lists[(size_t)(i / K) * WS_NQS * K + (size_t)qs * K + (i % K)] = ~0ull;
             } else {
                 u64* qlist = lists + (size_t)qs * 2 * K;
@@ -978,7 +989,7 @@ __device__ __forceinline__ void ws_job_end(const ScanArgs& a, const WsJob* J, Ws
         }
     }
     __syncwarp();
-    nbar_arrive(WS_BAR_EMPTY0 + slot, WS_BAR_EMPTY_N);
+    nbar_arrive(WS_BAR_EMPTY0 + slot, C::BAR_EMPTY_N);
 }
 
 // Scanner warp main loop.  Per pair: the 2 x min(nch, 4) chunk registers of
@@ -989,7 +1000,7 @@ __device__ __forceinline__ void ws_job_end(const ScanArgs& a, const WsJob* J, Ws
 // comes from the same job, else from the next job if its LUTs are already
 // built.  NCH > 0: the chunk count s_pad/16 as a compile-time constant (the
 // BASELINE shapes; straight-line code), 0: read from the arguments.
-template <int DT, int LOGN, int NCH, bool CH>
+template <class C, int DT, int LOGN, int NCH, bool CH>
 __device__ void ws_scanner(const ScanArgs& a, const WsArgs& w, WsJob* jobs, int* cnt, u64* full, int NBUF,
                            WsQuery* qst, u64* lists, int K, uint32_t lut_s0, uint32_t slot_bytes, uint32_t lut_each,
                            WarpTopK& tk, u64* qfree, int sw, int lane) {
@@ -1001,7 +1012,7 @@ __device__ void ws_scanner(const ScanArgs& a, const WsArgs& w, WsJob* jobs, int*
     const int nch = NCH > 0 ? NCH : w.rcc;
     const int rcc = w.rcc, nh = w.nh;
     // chunked: this warp's partial sums, 64 floats (32 lanes x 2 vectors) per owned pair
-    u64* part = CH ? reinterpret_cast<u64*>(w.part) + ((size_t)blockIdx.x * WS_SW + sw) * w.maxp * 32 + lane : nullptr;
+    u64* part = CH ? reinterpret_cast<u64*>(w.part) + ((size_t)blockIdx.x * C::SW + sw) * w.maxp * 32 + lane : nullptr;
     const int s_pad = a.s_pad;
     u64 pol;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
@@ -1014,7 +1025,7 @@ __device__ void ws_scanner(const ScanArgs& a, const WsArgs& w, WsJob* jobs, int*
     mbar_wait(full, 0);
     if (jobs[0].qs < 0) return;
     ct.load(jobs, lane, sw);
-    bool have = ws_grab<CH>(ct, cnt, 0, lut_s0, lut_each, codes, s_pad, rcc, lane, cur);
+    bool have = ws_grab<C, CH>(ct, cnt, 0, lut_s0, lut_each, codes, s_pad, rcc, lane, cur);
     auto load_first = [&](const WsPair& p) {
 #pragma unroll
         for (int u = 0; u < NS; ++u)
@@ -1028,7 +1039,7 @@ __device__ void ws_scanner(const ScanArgs& a, const WsArgs& w, WsJob* jobs, int*
     if (have) load_first(cur);
     while (true) {
         if (!have) {
-            ws_job_end(a, jobs + slot, qst, lists, K, tk, qfree, slot, lane);
+            ws_job_end<C>(a, jobs + slot, qst, lists, K, tk, qfree, slot, lane);
             if (++slot == NBUF) {
                 slot = 0;
                 ph ^= 1;
@@ -1036,13 +1047,13 @@ __device__ void ws_scanner(const ScanArgs& a, const WsArgs& w, WsJob* jobs, int*
             mbar_wait(full + slot, ph);
             if (jobs[slot].qs < 0) break;
             ct.load(jobs + slot, lane, sw);
-            have = ws_grab<CH>(ct, cnt, slot, lut_s0 + (uint32_t)slot * slot_bytes, lut_each, codes, s_pad, rcc, lane,
+            have = ws_grab<C, CH>(ct, cnt, slot, lut_s0 + (uint32_t)slot * slot_bytes, lut_each, codes, s_pad, rcc, lane,
                                cur);
             if (have) load_first(cur);
             continue;
         }
         // ---- the next pair: same job, else the next job if its LUTs are ready
-        bool hn = ws_grab<CH>(ct, cnt, slot, lut_s0 + (uint32_t)slot * slot_bytes, lut_each, codes, s_pad, rcc, lane,
+        bool hn = ws_grab<C, CH>(ct, cnt, slot, lut_s0 + (uint32_t)slot * slot_bytes, lut_each, codes, s_pad, rcc, lane,
                               nxt);
         bool cross = false;
         if (!hn) {
@@ -1052,7 +1063,7 @@ __device__ void ws_scanner(const ScanArgs& a, const WsArgs& w, WsJob* jobs, int*
             // test as complete, so there is no cross-job prefetch)
             if (NBUF > 1 && mbar_test(full + ns, (uint32_t)nph) && jobs[ns].qs >= 0) {
                 nt.load(jobs + ns, lane, sw);
-                hn = ws_grab<CH>(nt, cnt, ns, lut_s0 + (uint32_t)ns * slot_bytes, lut_each, codes, s_pad, rcc, lane,
+                hn = ws_grab<C, CH>(nt, cnt, ns, lut_s0 + (uint32_t)ns * slot_bytes, lut_each, codes, s_pad, rcc, lane,
                                  nxt);
                 cross = true;  // (an empty next job is left to the blocking path)
             }
@@ -1067,7 +1078,7 @@ __device__ void ws_scanner(const ScanArgs& a, const WsArgs& w, WsJob* jobs, int*
         const uint32_t base0 = cur.base0, base1 = cur.base1;
         u64 acc = pk2(0.f, 0.f);
         // chunked: continue the sums of this pair's earlier row chunks (sequential in j)
-        if (CH && cur.h > 0) acc = part[(size_t)((cur.k - sw) / WS_SW) * 32];
+        if (CH && cur.h > 0) acc = part[(size_t)((cur.k - sw) / C::SW) * 32];
 #pragma unroll(NCH > 0 ? 1 : 1)
         for (int cg = 0; cg < nch; cg += 4) {
 #pragma unroll
@@ -1084,7 +1095,7 @@ __device__ void ws_scanner(const ScanArgs& a, const WsArgs& w, WsJob* jobs, int*
         }
         // ---- offers against the query's shared threshold (chunked: after the last chunk)
         if (CH && cur.h < nh - 1) {
-            part[(size_t)((cur.k - sw) / WS_SW) * 32] = acc;
+            part[(size_t)((cur.k - sw) / C::SW) * 32] = acc;
         } else {
             float r0, r1;
             upk2(acc, r0, r1);
@@ -1103,7 +1114,7 @@ __device__ void ws_scanner(const ScanArgs& a, const WsArgs& w, WsJob* jobs, int*
             continue;
         }
         if (cross) {  // this warp's part of the current job is done
-            ws_job_end(a, jobs + slot, qst, lists, K, tk, qfree, slot, lane);
+            ws_job_end<C>(a, jobs + slot, qst, lists, K, tk, qfree, slot, lane);
             if (++slot == NBUF) {
                 slot = 0;
                 ph ^= 1;
@@ -1246,17 +1257,17 @@ __global__ void __launch_bounds__(256) ws_plan_kernel(const ScanArgs a, int G, i
 }
 #endif
 
-template <int DT, int LOGN, int SUB_D, bool GMEM, int NCH, bool CH>
-__global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) {
+template <class C, int DT, int LOGN, int SUB_D, bool GMEM, int NCH, bool CH>
+__global__ void __launch_bounds__(C::THREADS, 1) scan_ws_kernel(const WsArgs w) {
     using T = typename LutTraits<DT>::T;
     extern __shared__ __align__(1024) uint8_t ws_smem[];
     uint8_t* smem = ws_smem;
     const ScanArgs& a = w.a;
     const int G = a.G, NBUF = w.NBUF, K = a.K, NQS = WS_NQS;
-    const WsLayout L(a.d, a.s, SUB_D, LOGN, (int)sizeof(T), G, NBUF, K, a.s_pad, CH ? w.rc : 0);
+    const WsLayout<C> L(a.d, a.s, SUB_D, LOGN, (int)sizeof(T), G, NBUF, K, a.s_pad, CH ? w.rc : 0);
     const size_t lut_each = L.lut_each;
     const int d_pad = (int)L.d_pad;  // residual floats per list in a job (chunked: the chunk's rows)
-    constexpr int RB = WsBuild<DT, LOGN, SUB_D, GMEM>::R;
+    constexpr int RB = WsBuild<C, DT, LOGN, SUB_D, GMEM>::R;
     const int jpt = CH ? w.rc / RB : (a.s_pad + RB - 1) / RB;  // owned rows per builder thread per job
     u64* pfull = reinterpret_cast<u64*>(smem + L.bars);  // pfull[PD]: job + residuals prepared (TMA tx)
     u64* full = pfull + WS_PD;                            // full[NBUF]: LUTs ready
@@ -1270,7 +1281,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
     if ((smem_addr(lut_all) & 255u) != 0u) __trap();  // PRMT LUT addressing needs 256-byte alignment
 
     // ---- setup
-    for (int i = threadIdx.x; i < (K <= WS_PRIV_K ? WS_SW * NQS * K : NQS * 2 * K); i += blockDim.x) lists[i] = ~0ull;
+    for (int i = threadIdx.x; i < (K <= WS_PRIV_K ? C::SW * NQS * K : NQS * 2 * K); i += blockDim.x) lists[i] = ~0ull;
     if (threadIdx.x < WS_NQS) {
         WsQuery* S = qst + threadIdx.x;
         S->tau = ~0ull;
@@ -1280,12 +1291,12 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
         S->cur = 0;
         S->q = -1;
     }
-    using Builder = WsBuild<DT, LOGN, SUB_D, GMEM>;
+    using Builder = WsBuild<C, DT, LOGN, SUB_D, GMEM>;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.tmem);
     if (warp == 0) tmem_alloc<Builder::NCOL>(smem_addr(tmem_slot));
     if (threadIdx.x == 0) {
         for (int b = 0; b < WS_PD; ++b) mbar_init(pfull + b, 1);
-        for (int b = 0; b < NBUF; ++b) mbar_init(full + b, WS_BW);
+        for (int b = 0; b < NBUF; ++b) mbar_init(full + b, C::BW);
         u64* qf = reinterpret_cast<u64*>(smem + L.qfree);
         for (int b = 0; b < WS_NQS; ++b) mbar_init(qf + b, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -1295,7 +1306,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
     tmem_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    if (warp == WS_PREP_WARP) {
+    if (warp == C::PREP) {
         // ============================ prep warp ============================
 
         // Hands out queries and streams their planned jobs (descriptor +
@@ -1310,7 +1321,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
             if (lane == 0) q = atomicAdd(w.work, 1);
             q = __shfl_sync(0xffffffffu, q, 0);
             if (q >= a.nq) {
-                if (job >= WS_PD) nbar_sync(WS_BAR_PEMPTY0 + ps, WS_BAR_PEMPTY_N);
+                if (job >= WS_PD) nbar_sync(WS_BAR_PEMPTY0 + ps, C::BAR_PEMPTY_N);
                 if (lane == 0) {
                     pqs[ps] = -1;
                     mbar_arrive(pfull + ps);
@@ -1329,7 +1340,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
                 S->ncand = w.plan_ncand[q];
             }
             for (int j = 0; j < nj; ++j, ++job) {
-                if (job >= WS_PD) nbar_sync(WS_BAR_PEMPTY0 + ps, WS_BAR_PEMPTY_N);
+                if (job >= WS_PD) nbar_sync(WS_BAR_PEMPTY0 + ps, C::BAR_PEMPTY_N);
                 if (lane == 0) {
                     pqs[ps] = qs;
                     const size_t gj = (size_t)q * w.JMAX + j;
@@ -1341,7 +1352,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
                 if (++ps == WS_PD) ps = 0;
             }
         }
-    } else if (warp < WS_BW) {
+    } else if (warp < C::BW) {
         // =========================== builders ===========================
 
         const int t = threadIdx.x;
@@ -1352,7 +1363,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
         for (;;) {
             mbar_wait(pfull + ps, pph);
             // the slot's previous job has been scanned by every scanner warp
-            if (wrapped) nbar_sync(WS_BAR_EMPTY0 + slot, WS_BAR_EMPTY_N);
+            if (wrapped) nbar_sync(WS_BAR_EMPTY0 + slot, C::BAR_EMPTY_N);
             const WsJob* PJ = pjobs + ps;
             const int pq_s = reinterpret_cast<const int*>(smem + L.prepq)[ps];
             WS_CHECK(pq_s >= -1 && pq_s < WS_NQS && (pq_s < 0 || (PJ->ng >= 1 && PJ->ng <= G && PJ->nblk >= PJ->ng)));
@@ -1387,7 +1398,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
                     lut_all + (size_t)slot * G * lut_each, (uint32_t)lut_each, PJ->ng, jpt, CH ? PJ->h * jpt : 0);
             __syncwarp();  // the warp's LUT stores / prep reads are ordered before its arrivals
             if (lane == 0) mbar_arrive(full + slot);
-            nbar_arrive(WS_BAR_PEMPTY0 + ps, WS_BAR_PEMPTY_N);
+            nbar_arrive(WS_BAR_PEMPTY0 + ps, C::BAR_PEMPTY_N);
             if (++ps == WS_PD) {
                 ps = 0;
                 pph ^= 1;
@@ -1397,15 +1408,15 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(const WsArgs w) 
                 wrapped = true;
             }
         }
-        bar_builders();  // every builder is done with TMEM
+        bar_builders<C::NB>();  // every builder is done with TMEM
         if (warp == 0) tmem_dealloc<Builder::NCOL>(tmem);
     } else {
         // =========================== scanners ===========================
 
-        const int sw = warp - WS_BW;
+        const int sw = warp - C::BW;
         u64* wb = reinterpret_cast<u64*>(smem + L.wbuf) + (size_t)sw * 2 * WS_WBUF;
         WarpTopK tk{wb, wb + WS_WBUF, 0, K <= WS_PRIV_K ? lists + (size_t)sw * WS_NQS * K : nullptr};
-        ws_scanner<DT, LOGN, NCH, CH>(a, w, jobs, reinterpret_cast<int*>(smem + L.cnt), full, NBUF, qst, lists, K,
+        ws_scanner<C, DT, LOGN, NCH, CH>(a, w, jobs, reinterpret_cast<int*>(smem + L.cnt), full, NBUF, qst, lists, K,
                                       smem_addr(lut_all), (uint32_t)(G * lut_each), (uint32_t)lut_each, tk,
                                       reinterpret_cast<u64*>(smem + L.qfree), sw, lane);
     }

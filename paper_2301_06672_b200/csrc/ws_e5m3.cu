@@ -2,7 +2,8 @@
 #include "ws_launch.cuh"
 
 namespace ivfpq {
-cudaError_t ws_launch_e5m3(int logn, int sub_d, const WsArgs& w, size_t smem, int grid, cudaStream_t st) {
-    return ws_launch_dt<LUT_E5M3>(logn, sub_d, w, smem, grid, st);
+cudaError_t ws_launch_e5m3(int layout, int logn, int sub_d, const WsArgs& w, size_t smem, int grid,
+                           cudaStream_t st) {
+    return ws_launch_dt<LUT_E5M3>(layout, logn, sub_d, w, smem, grid, st);
 }
 }  // namespace ivfpq

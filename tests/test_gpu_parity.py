@@ -23,14 +23,16 @@ def pkg():
     return p
 
 
-@pytest.fixture(params=["auto", "v1", "chunked"])
+@pytest.fixture(params=["auto", "v1", "chunked", "layoutA", "layoutB"])
 def scan_kernel(request, pkg):
     """Run a test with the persistent warp-specialised scan (auto), with the
-    per-query scan kernel (v1), and with the persistent kernel preferring
+    per-query scan kernel (v1), with the persistent kernel preferring
     row-chunked LUT jobs (partial sums carried between chunks) wherever the
-    shape allows them."""
+    shape allows them, and with each warp layout forced (A: 8 builder + 11
+    scanner warps; B: 4 + 15, built for the cfg4 / cfg5 / cfg3 p5 shapes)."""
     from paper_2301_06672_b200 import _lib
-    _lib.check(_lib.lib.ivfpq_set_scan_kernel({"auto": 0, "v1": 1, "chunked": 2}[request.param]))
+    mode = {"auto": 0, "v1": 1, "chunked": 2, "layoutA": 3, "layoutB": 4}[request.param]
+    _lib.check(_lib.lib.ivfpq_set_scan_kernel(mode))
     yield request.param
     _lib.check(_lib.lib.ivfpq_set_scan_kernel(0))
 
