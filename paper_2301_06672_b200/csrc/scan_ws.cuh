@@ -616,18 +616,6 @@ struct WsBuild {
             float f0, f1, f2, f3;
             upk2(y01, f0, f1);
             upk2(y23, f2, f3);
-#ifdef WS_ENC_I2IP
-            // code = min(bits >> (23-M), 255): four shifts, then two saturating
-            // packs (cvt.pack.sat.u8.s32 = I2IP) build the 4-byte word
-            uint32_t t, d;
-            asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;"
-                : "=r"(t)
-                : "r"(__float_as_uint(f3) >> (23 - M)), "r"(__float_as_uint(f2) >> (23 - M)), "r"(0u));
-            asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;"
-                : "=r"(d)
-                : "r"(__float_as_uint(f1) >> (23 - M)), "r"(__float_as_uint(f0) >> (23 - M)), "r"(t));
-            *reinterpret_cast<uint32_t*>(dst) = d;
-#else
             // code = min(bits >> (23-M), 255) = min(bits >> 16, lim) >> (7-M), two per u16x2
             constexpr uint32_t lim = (256u << (7 - M)) - 1u;  // 0x0FFF (m=3) / 0x07FF (m=4)
             uint32_t h01 = __byte_perm(__float_as_uint(f0), __float_as_uint(f1), 0x7632);
@@ -635,7 +623,6 @@ struct WsBuild {
             h01 = min_u16x2(h01, lim | (lim << 16)) >> (7 - M);
             h23 = min_u16x2(h23, lim | (lim << 16)) >> (7 - M);
             *reinterpret_cast<uint32_t*>(dst) = __byte_perm(h01, h23, 0x6420);
-#endif
         }
     }
 };
