@@ -669,6 +669,7 @@ int run_scan_ws(ivfpq_index* idx, ScanArgs a, int64_t nq, int64_t P, int64_t K, 
     w.NBUF = plan.NBUF;
     w.gmem = plan.gmem;
     w.l2pf = (int64_t)idx->n_local * idx->s_pad > idx->l2_bytes ? 1 : 0;
+    w.n_codes_bytes = (long long)idx->n_local * idx->s_pad;
     w.nh = plan.nh;
     w.rc = plan.nh > 1 ? plan.rc : 0;
     w.rcc = (int)(plan.nh > 1 ? plan.rc / 16 : idx->s_pad / 16);
@@ -773,11 +774,13 @@ int run_scan(ivfpq_index* idx, const float* d_q, int64_t nq, const uint64_t* d_p
     if (nq == 0) return IVFPQ_OK;
     // v2 (persistent, warp-specialised, codebook in tensor memory) when the
     // shape fits its register/smem budget; v1 otherwise.  Layout B (4 builder +
-    // 15 scanner warps) for scan-heavy shapes (>= 2 lookups per LUT entry on
-    // average: cfg4, cfg5, cfg3 p5), layout A (8 + 11) otherwise.
+    // 15 scanner warps) for scan-heavy shapes (>= 4 lookups per LUT entry on
+    // average: cfg5 ~6, cfg3 p5 ~7.6), layout A (8 + 11) otherwise.  Measured
+    // (scan ms, e5m3, A -> B): cfg5 48.4 -> 40.2, cfg3 p5 46.7 -> 38.6, but
+    // cfg4 (2.4 per entry, k = 100) 11.7 -> 13.2.
     const int mode = g_scan_mode.load();
     const double per_entry = (double)idx->n_local / (double)std::max<int64_t>(1, idx->nlist_local) / (double)(1 << idx->p);
-    const bool want_b = mode == 4 || (mode == 0 && per_entry >= 2.0);
+    const bool want_b = mode == 4 || (mode == 0 && per_entry >= 4.0);
     if (want_b && ws_layout_b_supported(idx)) {
         bool done = false;
         CKR(run_scan_ws<WsCfgB>(idx, a, nq, P, K, dt, st, 1, &done));

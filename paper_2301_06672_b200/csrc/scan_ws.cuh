@@ -60,10 +60,11 @@ namespace ivfpq {
 //  * WsCfgB = 4 + 15: scan-heavy shapes (cfg5: 8 KiB LUTs and ~10-20 lookups
 //    per entry; the 8 builder warps of layout A idle ~40% of the time there
 //    while the scanners wait on the code stream).
-template <int BW_, int SW_>
+template <int BW_, int SW_, bool SCAN_PF_>
 struct WsCfg {
     static constexpr int BW = BW_;                     // builder warps
     static constexpr int SW = SW_;                     // scanner warps
+    static constexpr bool SCAN_PF = SCAN_PF_;          // scanners bulk-prefetch codes ahead (code store > L2)
     static constexpr int NB = BW * 32;                 // builder threads
     static constexpr int PREP = BW + SW;               // the prep warp
     static constexpr int THREADS = (BW + SW + 1) * 32;
@@ -75,8 +76,8 @@ struct WsCfg {
     __host__ __device__ static constexpr int JPT(int sub_d) { return 64 / (sub_d * BW / 4); }
     static_assert(BW % 4 == 0, "builder warps fill TMEM lane quarters");
 };
-using WsCfgA = WsCfg<8, 11>;
-using WsCfgB = WsCfg<4, 15>;
+using WsCfgA = WsCfg<8, 11, false>;
+using WsCfgB = WsCfg<4, 15, true>;
 
 constexpr int WS_MAX_G = 8;
 constexpr int WS_MAX_NBUF = 6;
@@ -91,6 +92,7 @@ constexpr int WS_PD = 8;                     // prep ring depth (jobs prepared a
 constexpr int WS_WBUF = WS_WBUF_CFG;         // per-warp candidate buffer
 constexpr int WS_MAX_K = 512;
 constexpr int WS_PRIV_K = 32;                // K up to which every scanner warp keeps private top-k lists
+constexpr int WS_PF_PAIRS = 2;               // L2 prefetch distance, in rounds of pairs (x SW pairs)
 // Named barriers (16 per CTA; id 0 = __syncthreads):
 constexpr int WS_BAR_BUILD = 1;              // builders only (teardown)
 constexpr int WS_BAR_EMPTY0 = 2;             // + slot: LUT slot free   (builders sync, scanners arrive)
@@ -108,7 +110,8 @@ struct WsArgs {
     int JMAX;
     int NBUF;
     int gmem;              // 1: builders read the codebook from global memory (does not fit TMEM)
-    int l2pf;              // 1: builders bulk-prefetch each job's codes into L2 (code store > L2)
+    int l2pf;              // 1: codes are bulk-prefetched into L2 ahead of the scanners (code store > L2)
+    long long n_codes_bytes;  // size of the code store (prefetch bound)
     // Row-chunked LUTs (tables larger than the shared-memory budget, e.g. the
     // f32 LUT at s = 240, p = 8: 240 KiB): a group of G lists is processed as
     // nh consecutive jobs, job h holding LUT rows [h*rc, (h+1)*rc) = code
@@ -851,7 +854,8 @@ struct WsJobTab {
 // (in its own scratch) and chunk h+1 of a pair never starts before chunk h.
 template <class C, bool CH>
 __device__ __forceinline__ bool ws_grab(WsJobTab& T, int* cnt, int slot, uint32_t slot_base, uint32_t lut_each,
-                                        const uint8_t* codes, int s_pad, int rcc, int lane, WsPair& p) {
+                                        const uint8_t* codes, int s_pad, int rcc, int lane, WsPair& p,
+                                        const uint8_t* pf_end) {
     int k = 0;
     if constexpr (CH) {
         k = T.next;
@@ -861,6 +865,16 @@ __device__ __forceinline__ bool ws_grab(WsJobTab& T, int* cnt, int slot, uint32_
         k = __shfl_sync(0xffffffffu, k, 0);
     }
     if (2 * k >= T.nblk) return false;
+    if (C::SCAN_PF && !CH && pf_end != nullptr) {
+        // bulk L2 prefetch of the two blocks WS_PF_PAIRS rounds of pairs ahead
+        const int bf = 2 * (k + WS_PF_PAIRS * C::SW);
+        if (bf < T.nblk) {
+            int gf, nbf, vof;
+            T.block(bf, gf, nbf, vof);
+            const uint8_t* src = codes + (long long)vof * s_pad;
+            if (lane == 0) prefetch_l2(src, (uint32_t)min((long long)(64 * s_pad), (long long)(pf_end - src)));
+        }
+    }
     p.qs = T.qs;
     p.k = k;
     p.h = T.h;
@@ -1004,6 +1018,8 @@ __device__ void ws_scanner(const ScanArgs& a, const WsArgs& w, WsJob* jobs, int*
     u64 pol;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
     const uint8_t* codes = a.codes;
+    // end of the code store when the scanners bulk-prefetch into L2 (else null)
+    const uint8_t* pf_end = w.l2pf ? codes + (size_t)w.n_codes_bytes : nullptr;
     uint4 A[NS], B[NS];
     uint32_t idA = 0, idB = 0;
     int slot = 0, ph = 0;
@@ -1012,7 +1028,7 @@ __device__ void ws_scanner(const ScanArgs& a, const WsArgs& w, WsJob* jobs, int*
     mbar_wait(full, 0);
     if (jobs[0].qs < 0) return;
     ct.load(jobs, lane, sw);
-    bool have = ws_grab<C, CH>(ct, cnt, 0, lut_s0, lut_each, codes, s_pad, rcc, lane, cur);
+    bool have = ws_grab<C, CH>(ct, cnt, 0, lut_s0, lut_each, codes, s_pad, rcc, lane, cur, pf_end);
     auto load_first = [&](const WsPair& p) {
 #pragma unroll
         for (int u = 0; u < NS; ++u)
@@ -1035,13 +1051,13 @@ __device__ void ws_scanner(const ScanArgs& a, const WsArgs& w, WsJob* jobs, int*
             if (jobs[slot].qs < 0) break;
             ct.load(jobs + slot, lane, sw);
             have = ws_grab<C, CH>(ct, cnt, slot, lut_s0 + (uint32_t)slot * slot_bytes, lut_each, codes, s_pad, rcc, lane,
-                               cur);
+                               cur, pf_end);
             if (have) load_first(cur);
             continue;
         }
         // ---- the next pair: same job, else the next job if its LUTs are ready
         bool hn = ws_grab<C, CH>(ct, cnt, slot, lut_s0 + (uint32_t)slot * slot_bytes, lut_each, codes, s_pad, rcc, lane,
-                              nxt);
+                              nxt, pf_end);
         bool cross = false;
         if (!hn) {
             const int ns = slot + 1 == NBUF ? 0 : slot + 1;
@@ -1051,7 +1067,7 @@ __device__ void ws_scanner(const ScanArgs& a, const WsArgs& w, WsJob* jobs, int*
             if (NBUF > 1 && mbar_test(full + ns, (uint32_t)nph) && jobs[ns].qs >= 0) {
                 nt.load(jobs + ns, lane, sw);
                 hn = ws_grab<C, CH>(nt, cnt, ns, lut_s0 + (uint32_t)ns * slot_bytes, lut_each, codes, s_pad, rcc, lane,
-                                 nxt);
+                                 nxt, pf_end);
                 cross = true;  // (an empty next job is left to the blocking path)
             }
         }
@@ -1369,18 +1385,25 @@ __global__ void __launch_bounds__(C::THREADS, 1) scan_ws_kernel(const WsArgs w) 
                 if (lane == 0) mbar_arrive(full + slot);
                 break;
             }
-            // When the code store is larger than L2 (cfg5: 3.2 GB) the job's
-            // code ranges (one contiguous range per list in the interleaved
-            // layout) are pulled into L2 now, a job or more before the scanners
-            // reach them: their own register prefetch of one pair ahead does not
-            // cover the DRAM latency (cfg5 e5m3 scan 47.1 -> 44.5 ms; with an
-            // L2-resident store it only adds requests: cfg2 +1.7%, so off there).
-#ifdef WS_NO_L2PF  // (variant switch for experiments)
-            if (false)
-#else
-            if (w.l2pf && PJ->h == 0 && t < PJ->ng)
-#endif
-                prefetch_l2(a.codes + PJ->off[t] * a.s_pad, (uint32_t)PJ->len[t] * (uint32_t)a.s_pad);
+            // When the code store is larger than L2 (cfg5: 3.2 GB) the scanners'
+            // register prefetch of one pair ahead does not cover the DRAM
+            // latency, so codes are also pulled into L2 with bulk prefetches: the
+            // start of the job here (a list's codes are one contiguous range in
+            // the interleaved layout), the rest by the scanners, WS_PF_PAIRS
+            // rounds of pairs ahead of their grabs.  (Whole jobs prefetched NBUF
+            // jobs ahead overflowed L2 at cfg5: 225 GB of DRAM reads for 113 GB
+            // of codes.)  With an L2-resident store it only adds requests (cfg2
+            // +1.7%), so it is off there.
+            if (w.l2pf && PJ->h == 0 && t < PJ->ng) {
+                // only the job's first 2 * WS_PF_PAIRS(SW) blocks: the scanners
+                // prefetch the rest a fixed distance ahead of their grabs
+                const int win = 2 * WS_PF_PAIRS * C::SW;
+                const int b0 = PJ->pref[t], b1 = min(PJ->pref[t + 1], win);
+                if (b0 < b1) {
+                    const int nv = min(PJ->len[t], (b1 - b0) * 32);
+                    prefetch_l2(a.codes + PJ->off[t] * a.s_pad, (uint32_t)nv * (uint32_t)a.s_pad);
+                }
+            }
             B.build(reinterpret_cast<const uint8_t*>(prq) + (size_t)ps * G * d_pad * 4, (uint32_t)(d_pad * 4),
                     lut_all + (size_t)slot * G * lut_each, (uint32_t)lut_each, PJ->ng, jpt, CH ? PJ->h * jpt : 0);
             __syncwarp();  // the warp's LUT stores / prep reads are ordered before its arrivals
