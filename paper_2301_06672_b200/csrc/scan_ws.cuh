@@ -84,15 +84,21 @@ constexpr int WS_MAX_NBUF = 6;
 #ifndef WS_NQS_CFG
 #define WS_NQS_CFG 4
 #endif
-constexpr int WS_NQS = WS_NQS_CFG;           // per-query states (query top-k lists) in flight
+constexpr int WS_NQS = WS_NQS_CFG;           // per-query states (query top-k lists) in flight, at most
+// query states in flight for k: 4, or 2 when the private per-warp lists are long (k > 32)
+__host__ __device__ constexpr int ws_nqs(int K) { return K <= 32 ? WS_NQS : 2; }
 constexpr int WS_PD = 8;                     // prep ring depth (jobs prepared ahead)
 #ifndef WS_WBUF_CFG
 #define WS_WBUF_CFG 64
 #endif
 constexpr int WS_WBUF = WS_WBUF_CFG;         // per-warp candidate buffer
 constexpr int WS_MAX_K = 512;
-constexpr int WS_PRIV_K = 32;                // K up to which every scanner warp keeps private top-k lists
+constexpr int WS_PRIV_K = 128;               // K up to which every scanner warp keeps private top-k lists
 constexpr int WS_PF_PAIRS = 2;               // L2 prefetch distance, in rounds of pairs (x SW pairs)
+// per-warp candidate buffer + sort scratch, each: WBUF keys, or K in the
+// private mode (a merged list is written there)
+__host__ __device__ constexpr int ws_wsz(int K) { return K <= WS_PRIV_K && K > WS_WBUF ? K : WS_WBUF; }
+
 // Named barriers (16 per CTA; id 0 = __syncthreads):
 constexpr int WS_BAR_BUILD = 1;              // builders only (teardown)
 constexpr int WS_BAR_EMPTY0 = 2;             // + slot: LUT slot free   (builders sync, scanners arrive)
@@ -383,10 +389,10 @@ struct WsLayout {
         qst = prepq + WS_PD * 4;                                          // WsQuery[NQS]
         qst = (qst + 15) & ~(size_t)15;
         lists = qst + WS_NQS * sizeof(WsQuery);                           // top-k lists (WarpTopK):
-        lists = (lists + 15) & ~(size_t)15;                               //  u64[SW][NQS][K] (K <= WS_PRIV_K)
-        wbuf = lists + (size_t)(K <= WS_PRIV_K ? C::SW * WS_NQS * K : WS_NQS * 2 * K) * 8;  // or u64[NQS][2][K]
-        //                                                                   u64[SW][2][WBUF]
-        prq = wbuf + (size_t)C::SW * 2 * WS_WBUF * 8;                     // f32[PD][G][d_pad] (TMA-filled)
+        lists = (lists + 15) & ~(size_t)15;                               //  u64[SW][nqs][K] (K <= WS_PRIV_K)
+        wbuf = lists + (size_t)(K <= WS_PRIV_K ? C::SW * ws_nqs(K) * K : WS_NQS * 2 * K) * 8;  // or [NQS][2][K]
+        //                                                                   u64[SW][2][wsz]
+        prq = wbuf + (size_t)C::SW * 2 * ws_wsz(K) * 8;                   // f32[PD][G][d_pad] (TMA-filled)
         prq = (prq + 127) & ~(size_t)127;
         lut = prq + (size_t)WS_PD * G * d_pad * 4;                        // [NBUF][G][lut_each]
         lut = (lut + 255) & ~(size_t)255;
@@ -633,14 +639,14 @@ struct WsBuild {
 // ------------------------------------------------------------- warp top-k
 // Top-k state per query.  Two layouts, chosen by K at launch:
 //  * K <= WS_PRIV_K ("private"): every scanner warp keeps its OWN sorted top-K
-//    per query state (lists[warp][qs][K]); a flush merges the warp's buffer
+//    per query state (lists[warp][qs][K]; 2 query states in flight for K > 32); a flush merges the warp's buffer
 //    into it and publishes its K-th key with a shared atomicMin into the
 //    query's threshold tau.  tau = min over warps of their K-th key is a valid
 //    filter: a key >= some warp's K-th key has K (unique) keys below it.  No
 //    lock; at the query's end the last warp merges the SW private lists.
-//  * larger K: one shared double-buffered list per query (lists[qs][2][K])
-//    merged under a per-query lock (smem budget: SW x NQS x K keys would not
-//    fit next to the LUT slots).
+//  * larger K (up to WS_MAX_K): one shared double-buffered list per query
+//    (lists[qs][2][K]) merged under a per-query lock (smem budget: SW x K keys
+//    per query state would not fit next to the LUT slots).
 struct WarpTopK {
     u64* buf;      // WS_WBUF
     u64* srt;      // WS_WBUF
@@ -931,7 +937,7 @@ __device__ __forceinline__ void ws_job_end(const ScanArgs& a, const WsJob* J, Ws
             const u64* r;
             if (tk.priv) {
                 // merge the SW private lists of this query: running result in buf
-                const size_t wstride = (size_t)WS_NQS * K;
+                const size_t wstride = (size_t)ws_nqs(K) * K;
                 const u64* L0 = lists + (size_t)qs * K;
                 for (int i = lane; i < K; i += 32) tk.buf[i] = L0[i];
                 for (int w = 1; w < C::SW; ++w) {
@@ -974,7 +980,7 @@ __device__ __forceinline__ void ws_job_end(const ScanArgs& a, const WsJob* J, Ws
             __syncwarp();
             if (tk.priv) {
                 for (int i = lane; i < C::SW * K; i += 32)
-                    lists[(size_t)(i / K) * WS_NQS * K + (size_t)qs * K + (i % K)] = ~0ull;
+                    lists[(size_t)(i / K) * ws_nqs(K) * K + (size_t)qs * K + (i % K)] = ~0ull;
             } else {
                 u64* qlist = lists + (size_t)qs * 2 * K;
                 for (int i = lane; i < 2 * K; i += 32) qlist[i] = ~0ull;
@@ -1266,7 +1272,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) scan_ws_kernel(const WsArgs w) 
     extern __shared__ __align__(1024) uint8_t ws_smem[];
     uint8_t* smem = ws_smem;
     const ScanArgs& a = w.a;
-    const int G = a.G, NBUF = w.NBUF, K = a.K, NQS = WS_NQS;
+    const int G = a.G, NBUF = w.NBUF, K = a.K, NQS = ws_nqs(a.K);
     const WsLayout<C> L(a.d, a.s, SUB_D, LOGN, (int)sizeof(T), G, NBUF, K, a.s_pad, CH ? w.rc : 0);
     const size_t lut_each = L.lut_each;
     const int d_pad = (int)L.d_pad;  // residual floats per list in a job (chunked: the chunk's rows)
@@ -1285,7 +1291,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) scan_ws_kernel(const WsArgs w) 
 
     // ---- setup
     for (int i = threadIdx.x; i < (K <= WS_PRIV_K ? C::SW * NQS * K : NQS * 2 * K); i += blockDim.x) lists[i] = ~0ull;
-    if (threadIdx.x < WS_NQS) {
+    if (threadIdx.x < NQS) {
         WsQuery* S = qst + threadIdx.x;
         S->tau = ~0ull;
         S->ncand = 0;
@@ -1301,7 +1307,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) scan_ws_kernel(const WsArgs w) 
         for (int b = 0; b < WS_PD; ++b) mbar_init(pfull + b, 1);
         for (int b = 0; b < NBUF; ++b) mbar_init(full + b, C::BW);
         u64* qf = reinterpret_cast<u64*>(smem + L.qfree);
-        for (int b = 0; b < WS_NQS; ++b) mbar_init(qf + b, 1);
+        for (int b = 0; b < NQS; ++b) mbar_init(qf + b, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     tmem_fence_before();
@@ -1369,7 +1375,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) scan_ws_kernel(const WsArgs w) 
             if (wrapped) nbar_sync(WS_BAR_EMPTY0 + slot, C::BAR_EMPTY_N);
             const WsJob* PJ = pjobs + ps;
             const int pq_s = reinterpret_cast<const int*>(smem + L.prepq)[ps];
-            WS_CHECK(pq_s >= -1 && pq_s < WS_NQS && (pq_s < 0 || (PJ->ng >= 1 && PJ->ng <= G && PJ->nblk >= PJ->ng)));
+            WS_CHECK(pq_s >= -1 && pq_s < NQS && (pq_s < 0 || (PJ->ng >= 1 && PJ->ng <= G && PJ->nblk >= PJ->ng)));
             if (t < 32) {  // the descriptor travels with the LUT slot (warp 0 copies it)
                 const int* src = reinterpret_cast<const int*>(PJ);
                 int* dst = reinterpret_cast<int*>(jobs + slot);
@@ -1424,8 +1430,9 @@ __global__ void __launch_bounds__(C::THREADS, 1) scan_ws_kernel(const WsArgs w) 
         // =========================== scanners ===========================
 
         const int sw = warp - C::BW;
-        u64* wb = reinterpret_cast<u64*>(smem + L.wbuf) + (size_t)sw * 2 * WS_WBUF;
-        WarpTopK tk{wb, wb + WS_WBUF, 0, K <= WS_PRIV_K ? lists + (size_t)sw * WS_NQS * K : nullptr};
+        const int wsz = ws_wsz(K);
+        u64* wb = reinterpret_cast<u64*>(smem + L.wbuf) + (size_t)sw * 2 * wsz;
+        WarpTopK tk{wb, wb + wsz, 0, K <= WS_PRIV_K ? lists + (size_t)sw * NQS * K : nullptr};
         ws_scanner<C, DT, LOGN, NCH, CH>(a, w, jobs, reinterpret_cast<int*>(smem + L.cnt), full, NBUF, qst, lists, K,
                                       smem_addr(lut_all), (uint32_t)(G * lut_each), (uint32_t)lut_each, tk,
                                       reinterpret_cast<u64*>(smem + L.qfree), sw, lane);
