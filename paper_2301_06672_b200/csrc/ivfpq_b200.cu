@@ -670,6 +670,8 @@ int run_scan_ws(ivfpq_index* idx, ScanArgs a, int64_t nq, int64_t P, int64_t K, 
     w.gmem = plan.gmem;
     w.l2pf = (int64_t)idx->n_local * idx->s_pad > idx->l2_bytes ? 1 : 0;
     w.n_codes_bytes = (long long)idx->n_local * idx->s_pad;
+    w.nqs = ws_nqs((int)K);
+    w.wsz = ws_wsz((int)K);
     w.nh = plan.nh;
     w.rc = plan.nh > 1 ? plan.rc : 0;
     w.rcc = (int)(plan.nh > 1 ? plan.rc / 16 : idx->s_pad / 16);

@@ -118,6 +118,8 @@ struct WsArgs {
     int gmem;              // 1: builders read the codebook from global memory (does not fit TMEM)
     int l2pf;              // 1: codes are bulk-prefetched into L2 ahead of the scanners (code store > L2)
     long long n_codes_bytes;  // size of the code store (prefetch bound)
+    int nqs;               // query states in flight (ws_nqs(K)), from the host
+    int wsz;               // per-warp candidate buffer / sort scratch keys (ws_wsz(K)), from the host
     // Row-chunked LUTs (tables larger than the shared-memory budget, e.g. the
     // f32 LUT at s = 240, p = 8: 240 KiB): a group of G lists is processed as
     // nh consecutive jobs, job h holding LUT rows [h*rc, (h+1)*rc) = code
@@ -937,7 +939,7 @@ __device__ __forceinline__ void ws_job_end(const ScanArgs& a, const WsJob* J, Ws
             const u64* r;
             if (tk.priv) {
                 // merge the SW private lists of this query: running result in buf
-                const size_t wstride = (size_t)ws_nqs(K) * K;
+                const size_t wstride = (size_t)ws_nqs(K) * K;  // (= w.nqs * K)
                 const u64* L0 = lists + (size_t)qs * K;
                 for (int i = lane; i < K; i += 32) tk.buf[i] = L0[i];
                 for (int w = 1; w < C::SW; ++w) {
@@ -1272,7 +1274,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) scan_ws_kernel(const WsArgs w) 
     extern __shared__ __align__(1024) uint8_t ws_smem[];
     uint8_t* smem = ws_smem;
     const ScanArgs& a = w.a;
-    const int G = a.G, NBUF = w.NBUF, K = a.K, NQS = ws_nqs(a.K);
+    const int G = a.G, NBUF = w.NBUF, K = a.K, NQS = w.nqs;
     const WsLayout<C> L(a.d, a.s, SUB_D, LOGN, (int)sizeof(T), G, NBUF, K, a.s_pad, CH ? w.rc : 0);
     const size_t lut_each = L.lut_each;
     const int d_pad = (int)L.d_pad;  // residual floats per list in a job (chunked: the chunk's rows)
@@ -1430,7 +1432,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) scan_ws_kernel(const WsArgs w) 
         // =========================== scanners ===========================
 
         const int sw = warp - C::BW;
-        const int wsz = ws_wsz(K);
+        const int wsz = w.wsz;
         u64* wb = reinterpret_cast<u64*>(smem + L.wbuf) + (size_t)sw * 2 * wsz;
         WarpTopK tk{wb, wb + wsz, 0, K <= WS_PRIV_K ? lists + (size_t)sw * NQS * K : nullptr};
         ws_scanner<C, DT, LOGN, NCH, CH>(a, w, jobs, reinterpret_cast<int*>(smem + L.cnt), full, NBUF, qst, lists, K,
