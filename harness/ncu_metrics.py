@@ -30,7 +30,7 @@ def load(path):
     rows = list(csv.DictReader(lines[start:]))
     per = defaultdict(dict)
     for r in rows:
-        m = re.search(r"scan_ws_kernel<(\d+),", r["Kernel Name"])
+        m = re.search(r"scan_ws_kernel<(?:WsCfg<[^>]*>, )?(\d+),", r["Kernel Name"])
         if not m:
             continue
         key = (r["ID"], DT_OF[m.group(1)])
