@@ -1048,9 +1048,16 @@ __device__ void ws_scanner(const ScanArgs& a, const WsArgs& w, WsJob* jobs, int*
         idB = lane < p.nb1 ? __ldg(a.ids + p.vo1 + lane) : 0u;
     };
     if (have) load_first(cur);
+    // A finished job is ended at the top of the next iteration (one inlined
+    // copy of ws_job_end: two copies pushed the pair loop into spilling), before
+    // any offer for another job and before blocking on the next slot.
+    int ended = have ? -1 : 0;
     while (true) {
+        if (ended >= 0) {
+            ws_job_end<C>(a, jobs + ended, qst, lists, K, tk, qfree, ended, lane);
+            ended = -1;
+        }
         if (!have) {
-            ws_job_end<C>(a, jobs + slot, qst, lists, K, tk, qfree, slot, lane);
             if (++slot == NBUF) {
                 slot = 0;
                 ph ^= 1;
@@ -1061,6 +1068,7 @@ __device__ void ws_scanner(const ScanArgs& a, const WsArgs& w, WsJob* jobs, int*
             have = ws_grab<C, CH>(ct, cnt, slot, lut_s0 + (uint32_t)slot * slot_bytes, lut_each, codes, s_pad, rcc, lane,
                                cur, pf_end);
             if (have) load_first(cur);
+            else ended = slot;  // no pair of this job for this warp
             continue;
         }
         // ---- the next pair: same job, else the next job if its LUTs are ready
@@ -1122,10 +1130,11 @@ __device__ void ws_scanner(const ScanArgs& a, const WsArgs& w, WsJob* jobs, int*
         }
         if (!hn) {
             have = false;
+            ended = slot;
             continue;
         }
         if (cross) {  // this warp's part of the current job is done
-            ws_job_end<C>(a, jobs + slot, qst, lists, K, tk, qfree, slot, lane);
+            ended = slot;
             if (++slot == NBUF) {
                 slot = 0;
                 ph ^= 1;
