@@ -529,7 +529,10 @@ struct WsBuild {
             float rA[SUB_D], rB[SUB_D];
             load_rq(raA, rA);
             load_rq(raB, rB);
-#pragma unroll 2
+#ifndef WS_GUNROLL
+#define WS_GUNROLL 2
+#endif
+#pragma unroll WS_GUNROLL
             for (int g = 0; g < ng; ++g) {
                 float nA[SUB_D], nB[SUB_D];
                 load_rq(raA + (g + 1) * rq_stride, nA);
