@@ -532,7 +532,8 @@ struct WsBuild {
 #ifndef WS_GUNROLL
 #define WS_GUNROLL 2
 #endif
-#pragma unroll WS_GUNROLL
+            constexpr int kGU = WS_GUNROLL;  // lists per unrolled step (experiment knob)
+#pragma unroll kGU
             for (int g = 0; g < ng; ++g) {
                 float nA[SUB_D], nB[SUB_D];
                 load_rq(raA + (g + 1) * rq_stride, nA);
