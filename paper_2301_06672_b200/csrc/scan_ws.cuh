@@ -923,7 +923,7 @@ __device__ __forceinline__ uint4 ws_ld(const uint8_t* p, u64 pol) {
 // End of this warp's part of the job in `slot`: at the query's last job, merge
 // the warp's candidates and let the last warp write the results and free the
 // query state; then release the LUT slot (named barrier, see the header).
-template <class C>
+template <class C, bool SMALLK>
 __device__ __forceinline__ void ws_job_end(const ScanArgs& a, const WsJob* J, WsQuery* qst, u64* lists, int K,
                                            WarpTopK& tk, u64* qfree, int slot, int lane) {
     if (J->last) {
@@ -943,7 +943,7 @@ __device__ __forceinline__ void ws_job_end(const ScanArgs& a, const WsJob* J, Ws
             const u64* r;
             if (tk.priv) {
                 // merge the SW private lists of this query: running result in buf
-                const size_t wstride = (size_t)ws_nqs(K) * K;  // (= w.nqs * K)
+                const size_t wstride = (size_t)(SMALLK ? WS_NQS : ws_nqs(K)) * K;
                 const u64* L0 = lists + (size_t)qs * K;
                 for (int i = lane; i < K; i += 32) tk.buf[i] = L0[i];
                 for (int w = 1; w < C::SW; ++w) {
@@ -986,7 +986,7 @@ __device__ __forceinline__ void ws_job_end(const ScanArgs& a, const WsJob* J, Ws
             __syncwarp();
             if (tk.priv) {
                 for (int i = lane; i < C::SW * K; i += 32)
-                    lists[(size_t)(i / K) * ws_nqs(K) * K + (size_t)qs * K + (i % K)] = ~0ull;
+                    lists[(size_t)(i / K) * (SMALLK ? WS_NQS : ws_nqs(K)) * K + (size_t)qs * K + (i % K)] = ~0ull;
             } else {
                 u64* qlist = lists + (size_t)qs * 2 * K;
                 for (int i = lane; i < 2 * K; i += 32) qlist[i] = ~0ull;
@@ -1013,7 +1013,7 @@ __device__ __forceinline__ void ws_job_end(const ScanArgs& a, const WsJob* J, Ws
 // comes from the same job, else from the next job if its LUTs are already
 // built.  NCH > 0: the chunk count s_pad/16 as a compile-time constant (the
 // BASELINE shapes; straight-line code), 0: read from the arguments.
-template <class C, int DT, int LOGN, int NCH, bool CH>
+template <class C, int DT, int LOGN, int NCH, bool CH, bool SMALLK>
 __device__ void ws_scanner(const ScanArgs& a, const WsArgs& w, WsJob* jobs, int* cnt, u64* full, int NBUF,
                            WsQuery* qst, u64* lists, int K, uint32_t lut_s0, uint32_t slot_bytes, uint32_t lut_each,
                            WarpTopK& tk, u64* qfree, int sw, int lane) {
@@ -1052,16 +1052,9 @@ __device__ void ws_scanner(const ScanArgs& a, const WsArgs& w, WsJob* jobs, int*
         idB = lane < p.nb1 ? __ldg(a.ids + p.vo1 + lane) : 0u;
     };
     if (have) load_first(cur);
-    // A finished job is ended at the top of the next iteration (one inlined
-    // copy of ws_job_end: two copies pushed the pair loop into spilling), before
-    // any offer for another job and before blocking on the next slot.
-    int ended = have ? -1 : 0;
     while (true) {
-        if (ended >= 0) {
-            ws_job_end<C>(a, jobs + ended, qst, lists, K, tk, qfree, ended, lane);
-            ended = -1;
-        }
         if (!have) {
+            ws_job_end<C, SMALLK>(a, jobs + slot, qst, lists, K, tk, qfree, slot, lane);
             if (++slot == NBUF) {
                 slot = 0;
                 ph ^= 1;
@@ -1072,7 +1065,6 @@ __device__ void ws_scanner(const ScanArgs& a, const WsArgs& w, WsJob* jobs, int*
             have = ws_grab<C, CH>(ct, cnt, slot, lut_s0 + (uint32_t)slot * slot_bytes, lut_each, codes, s_pad, rcc, lane,
                                cur, pf_end);
             if (have) load_first(cur);
-            else ended = slot;  // no pair of this job for this warp
             continue;
         }
         // ---- the next pair: same job, else the next job if its LUTs are ready
@@ -1134,11 +1126,10 @@ __device__ void ws_scanner(const ScanArgs& a, const WsArgs& w, WsJob* jobs, int*
         }
         if (!hn) {
             have = false;
-            ended = slot;
             continue;
         }
         if (cross) {  // this warp's part of the current job is done
-            ended = slot;
+            ws_job_end<C, SMALLK>(a, jobs + slot, qst, lists, K, tk, qfree, slot, lane);
             if (++slot == NBUF) {
                 slot = 0;
                 ph ^= 1;
@@ -1281,13 +1272,15 @@ __global__ void __launch_bounds__(256) ws_plan_kernel(const ScanArgs a, int G, i
 }
 #endif
 
-template <class C, int DT, int LOGN, int SUB_D, bool GMEM, int NCH, bool CH>
+// SMALLK: k <= 32 (the common case): query-state count and warp scratch are
+// compile-time constants (the runtime forms cost the cfg2 kernel ~4%: spills).
+template <class C, int DT, int LOGN, int SUB_D, bool GMEM, int NCH, bool CH, bool SMALLK>
 __global__ void __launch_bounds__(C::THREADS, 1) scan_ws_kernel(const WsArgs w) {
     using T = typename LutTraits<DT>::T;
     extern __shared__ __align__(1024) uint8_t ws_smem[];
     uint8_t* smem = ws_smem;
     const ScanArgs& a = w.a;
-    const int G = a.G, NBUF = w.NBUF, K = a.K, NQS = w.nqs;
+    const int G = a.G, NBUF = w.NBUF, K = a.K, NQS = SMALLK ? WS_NQS : w.nqs;
     const WsLayout<C> L(a.d, a.s, SUB_D, LOGN, (int)sizeof(T), G, NBUF, K, a.s_pad, CH ? w.rc : 0);
     const size_t lut_each = L.lut_each;
     const int d_pad = (int)L.d_pad;  // residual floats per list in a job (chunked: the chunk's rows)
@@ -1305,7 +1298,8 @@ __global__ void __launch_bounds__(C::THREADS, 1) scan_ws_kernel(const WsArgs w) 
     if ((smem_addr(lut_all) & 255u) != 0u) __trap();  // PRMT LUT addressing needs 256-byte alignment
 
     // ---- setup
-    for (int i = threadIdx.x; i < (K <= WS_PRIV_K ? C::SW * NQS * K : NQS * 2 * K); i += blockDim.x) lists[i] = ~0ull;
+    for (int i = threadIdx.x; i < (SMALLK || K <= WS_PRIV_K ? C::SW * NQS * K : NQS * 2 * K); i += blockDim.x)
+        lists[i] = ~0ull;
     if (threadIdx.x < NQS) {
         WsQuery* S = qst + threadIdx.x;
         S->tau = ~0ull;
@@ -1445,10 +1439,10 @@ __global__ void __launch_bounds__(C::THREADS, 1) scan_ws_kernel(const WsArgs w) 
         // =========================== scanners ===========================
 
         const int sw = warp - C::BW;
-        const int wsz = w.wsz;
+        const int wsz = SMALLK ? WS_WBUF : w.wsz;
         u64* wb = reinterpret_cast<u64*>(smem + L.wbuf) + (size_t)sw * 2 * wsz;
-        WarpTopK tk{wb, wb + wsz, 0, K <= WS_PRIV_K ? lists + (size_t)sw * NQS * K : nullptr};
-        ws_scanner<C, DT, LOGN, NCH, CH>(a, w, jobs, reinterpret_cast<int*>(smem + L.cnt), full, NBUF, qst, lists, K,
+        WarpTopK tk{wb, wb + wsz, 0, SMALLK || K <= WS_PRIV_K ? lists + (size_t)sw * NQS * K : nullptr};
+        ws_scanner<C, DT, LOGN, NCH, CH, SMALLK>(a, w, jobs, reinterpret_cast<int*>(smem + L.cnt), full, NBUF, qst, lists, K,
                                       smem_addr(lut_all), (uint32_t)(G * lut_each), (uint32_t)lut_each, tk,
                                       reinterpret_cast<u64*>(smem + L.qfree), sw, lane);
     }

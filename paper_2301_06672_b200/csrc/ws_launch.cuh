@@ -11,12 +11,12 @@ namespace ivfpq {
 
 // The dynamic-smem attribute is per device context, so it is set before every
 // launch (cheap) instead of once per process.
-template <class C, int DT, int LOGN, int SUB_D, bool GMEM, int NCH, bool CH = false>
+template <class C, int DT, int LOGN, int SUB_D, bool GMEM, int NCH, bool CH = false, bool SMALLK = true>
 cudaError_t ws_launch_k(const WsArgs& w, size_t smem, int grid, cudaStream_t st) {
-    cudaError_t e = cudaFuncSetAttribute(scan_ws_kernel<C, DT, LOGN, SUB_D, GMEM, NCH, CH>,
+    cudaError_t e = cudaFuncSetAttribute(scan_ws_kernel<C, DT, LOGN, SUB_D, GMEM, NCH, CH, SMALLK>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    scan_ws_kernel<C, DT, LOGN, SUB_D, GMEM, NCH, CH><<<grid, C::THREADS, smem, st>>>(w);
+    scan_ws_kernel<C, DT, LOGN, SUB_D, GMEM, NCH, CH, SMALLK><<<grid, C::THREADS, smem, st>>>(w);
     return cudaGetLastError();
 }
 
@@ -30,6 +30,21 @@ cudaError_t ws_launch_k(const WsArgs& w, size_t smem, int grid, cudaStream_t st)
 template <class C, int DT, int LOGN, int SUB_D, bool GMEM>
 cudaError_t ws_launch_g(const WsArgs& w, size_t smem, int grid, cudaStream_t st) {
     const int nch = w.a.s_pad >> 4;
+    // k > 32 (cfg4: k = 100): runtime top-k geometry, built for layout A only,
+    // the cfg4 shape specialised, every other shape the generic chunk loop
+    if (w.a.K > 32) {
+        if constexpr (std::is_same_v<C, WsCfgB>) {
+            return cudaErrorNotSupported;
+        } else {
+            if (w.nh > 1) {
+                if constexpr (LOGN >= 5) return ws_launch_k<C, DT, LOGN, SUB_D, GMEM, 0, true, false>(w, smem, grid, st);
+                return cudaErrorNotSupported;
+            }
+            if constexpr (LOGN == 8 && SUB_D == 2 && !GMEM)
+                if (nch == 3) return ws_launch_k<C, DT, LOGN, SUB_D, GMEM, 3, false, false>(w, smem, grid, st);
+            return ws_launch_k<C, DT, LOGN, SUB_D, GMEM, 0, false, false>(w, smem, grid, st);
+        }
+    }
     if constexpr (std::is_same_v<C, WsCfgB>) {
         if (w.nh == 1) {
             if constexpr (LOGN == 8 && SUB_D == 2 && !GMEM)
