@@ -31,16 +31,18 @@ from harness import cpu_build  # noqa: E402  (numpy only)
 # cfg5 re-calibrated with harness/calibrate.py (profiles/r02_calibration_*.jsonl):
 # the SURVEY proposals (64 / 1024 components, spread 0.3) put recall@10 at
 # 0.46 (cfg3 p8), 0.20 (cfg3 p5), 0.60 (cfg5) -- PQ-limited, not IVF-limited.
-# ~15 points per component (cfg3: 65536 comps, spread 0.15; cfg5: 6.55M comps,
-# spread 0.1) keeps the IVF ceiling responsive to nprobe and lifts recall@10
-# at the headline nprobe to ~0.83 (cfg3 p8), 0.78 (cfg3 p5), 0.84 (cfg5).
+# ~12-15 points per component (cfg3: 81920 comps, spread 0.15; cfg5: 6.55M
+# comps, spread 0.1) keeps the IVF ceiling responsive to nprobe (cfg3: 0.94 at
+# P 32) and lifts recall@10 at the headline nprobe above 0.8 (calibration
+# sample: 0.82 cfg3 p5, 0.84 cfg5; p5's 32 codewords cap it near 0.78 at
+# 65536 comps).
 CONFIGS = {
     "cfg1": dict(n=100_000, d=128, nlist=1024, s=64, p=8, nq=1_000, nprobe=32, k=10, comps=16, spread=0.3, seed=1),
     "cfg2": dict(n=1_000_000, d=128, nlist=4096, s=64, p=8, nq=10_000, nprobe=32, k=10, comps=64, spread=0.3,
                  seed=2),
-    "cfg3p8": dict(n=1_000_000, d=960, nlist=4096, s=240, p=8, nq=10_000, nprobe=32, k=10, comps=65536,
+    "cfg3p8": dict(n=1_000_000, d=960, nlist=4096, s=240, p=8, nq=10_000, nprobe=32, k=10, comps=81920,
                    spread=0.15, seed=3),
-    "cfg3p5": dict(n=1_000_000, d=960, nlist=4096, s=240, p=5, nq=10_000, nprobe=32, k=10, comps=65536,
+    "cfg3p5": dict(n=1_000_000, d=960, nlist=4096, s=240, p=5, nq=10_000, nprobe=32, k=10, comps=81920,
                    spread=0.15, seed=3),
     "cfg4": dict(n=10_000_000, d=96, nlist=16384, s=48, p=8, nq=10_000, nprobe=32, k=100, comps=256, spread=0.3,
                  seed=4),

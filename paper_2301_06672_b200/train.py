@@ -23,14 +23,13 @@ from .validation import check_matrix
 
 def _means(x, a, k, old):
     """Per-cluster means of rows x (n, m) under labels a; empty clusters keep
-    their previous centroid.  Float64 sums, deterministic (sort + prefix sums)."""
+    their previous centroid.  Float64 sums, deterministic: rows sorted by label,
+    then one sequential sum per (segment, column) (torch.segment_reduce; a
+    dim-0 cumsum of a tall, narrow matrix runs one thread per column)."""
     import torch
     order = torch.sort(a, stable=True).indices
-    cs = torch.zeros((x.shape[0] + 1, x.shape[1]), dtype=torch.float64, device=x.device)
-    cs[1:] = torch.cumsum(x[order].double(), 0)
     cnt = torch.bincount(a, minlength=k)
-    hi = torch.cumsum(cnt, 0)
-    sums = cs[hi] - cs[hi - cnt]
+    sums = torch.segment_reduce(x[order].double(), "sum", lengths=cnt, axis=0)
     return torch.where(cnt[:, None] > 0, (sums / cnt.clamp(min=1)[:, None]).float(), old)
 
 
