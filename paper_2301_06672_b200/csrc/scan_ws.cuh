@@ -5,7 +5,7 @@
 //
 //  * one CTA per SM (persistent), queries handed out by a global atomic;
 //  * the PQ codebook lives in TENSOR MEMORY (tcgen05.alloc/st/ld; up to 256 of
-//    the SM's 512 columns): each of the WS_BW = 8 BUILDER warps reads only its
+//    the SM's 512 columns): each of the BW BUILDER warps (8 in layout A, 4 in B) reads only its
 //    own lane's columns.  Builder thread t owns a quad of codes m = 4u..4u+3
 //    and the subspaces j = jr, jr+R, ... (u = t % (N/4), jr = t / (N/4),
 //    R = 4 * WS_NB / N); one tcgen05.ld of a row's centers serves all G lists
@@ -16,7 +16,7 @@
 //           min_normal become subnormal and flush to +0), then the code is
 //           min(bits >> (23-m), 255), done two-at-a-time with u16x2 min.
 //      f16: cvt.rn.satfinite.f16x2.f32 (= RNE of min(x, 65504)).
-//  * WS_SW = 11 SCANNER warps take pairs of 32-vector code blocks (16-byte
+//  * SW SCANNER warps (11 in layout A, 15 in B) take pairs of 32-vector code blocks (16-byte
 //    loads from L2 into registers, interleaved layout) and look the codes up
 //    in the slot's LUTs; R accumulates sequentially in j (fp32).
 //  * one PREP warp hands out queries and streams their planned jobs
@@ -29,8 +29,10 @@
 //    prep warp issued ~20% of all instructions of the kernel).
 //  * top-k: each scanner warp filters against the query's shared threshold and
 //    appends survivors to a private smem buffer; a full buffer is rank-sorted
-//    and merged into the query's shared sorted list under a per-query lock.
-//    The last warp to finish a query writes its results.
+//    and merged into the warp's PRIVATE sorted list (k <= 128), whose k-th key
+//    lowers the query's threshold with a shared atomicMin.  The last warp to
+//    finish a query merges the SW private lists and writes the results.
+//    k > 128: one shared list per query, merged under a per-query lock.
 #pragma once
 #include <stdint.h>
 
