@@ -646,7 +646,9 @@ bool ws_plan(const ivfpq_index* idx, int64_t P, int64_t K, int dt, WsPlan* plan)
 }
 
 // Shapes the layout-B kernels are built for (ws_launch.cuh): cfg4 (p 8, sub_d 2,
-// s 48), cfg5 (p 8, sub_d 3, s 32), cfg3 p5 (p 5, sub_d 4, s 240), codebook in TMEM.
+// s 48), cfg5 (p 8, sub_d 3, s 32), cfg3 p5 (p 5, sub_d 4, s 240), codebook in
+// TMEM.  (cfg3 p8 on layout B, codebook in global memory: 81.2 ms vs 78.8 on
+// A -- its 4 builder warps become the bottleneck; profiles/r02_scan_experiments.txt.)
 bool ws_layout_b_supported(const ivfpq_index* idx) {
     const int64_t nch = idx->s_pad / 16;
     if (idx->s_pad > WsCfgB::R((int)(1 << idx->p)) * WsCfgB::JPT((int)idx->sub_d)) return false;  // not TMEM
@@ -668,7 +670,15 @@ int run_scan_ws(ivfpq_index* idx, ScanArgs a, int64_t nq, int64_t P, int64_t K, 
     w.a = a;
     w.NBUF = plan.NBUF;
     w.gmem = plan.gmem;
-    w.l2pf = (int64_t)idx->n_local * idx->s_pad > idx->l2_bytes ? 1 : 0;
+    // code store larger than L2: builders prefetch each job's start; the
+    // scanners prefetch ahead of their grabs in layout B (IVFPQ_WS_SPF=0/1
+    // overrides the scanner part, for measurements)
+    static const int env_spf = [] {
+        const char* e = getenv("IVFPQ_WS_SPF");
+        return e ? atoi(e) : -1;
+    }();
+    const bool spf = env_spf >= 0 ? env_spf != 0 : C::SCAN_PF;
+    w.l2pf = (int64_t)idx->n_local * idx->s_pad > idx->l2_bytes ? (1 | (spf ? 2 : 0)) : 0;
     w.n_codes_bytes = (long long)idx->n_local * idx->s_pad;
     w.nqs = ws_nqs((int)K);
     w.wsz = ws_wsz((int)K);

@@ -96,6 +96,12 @@ constexpr int WS_PD = 8;                     // prep ring depth (jobs prepared a
 constexpr int WS_WBUF = WS_WBUF_CFG;         // per-warp candidate buffer
 constexpr int WS_MAX_K = 512;
 constexpr int WS_PRIV_K = 128;               // K up to which every scanner warp keeps private top-k lists
+#ifndef WS_PLAN_BALANCE
+#define WS_PLAN_BALANCE 0                    // 1: ws_plan_kernel groups a query's lists into length-balanced jobs (P <= 32); measured slower, see below
+#endif
+#ifndef WS_GMEM_PF
+#define WS_GMEM_PF 0                         // builders load global-memory codebook rows one iteration ahead (measured: no gain on layout A)
+#endif
 constexpr int WS_PF_PAIRS = 2;               // L2 prefetch distance, in rounds of pairs (x SW pairs)
 // per-warp candidate buffer + sort scratch, each: WBUF keys, or K in the
 // private mode (a merged list is written there)
@@ -118,7 +124,8 @@ struct WsArgs {
     int JMAX;
     int NBUF;
     int gmem;              // 1: builders read the codebook from global memory (does not fit TMEM)
-    int l2pf;              // 1: codes are bulk-prefetched into L2 ahead of the scanners (code store > L2)
+    int l2pf;              // code store > L2: bit 0 builders bulk-prefetch each job's start into L2,
+                           // bit 1 scanners prefetch WS_PF_PAIRS rounds of pairs ahead of their grabs
     long long n_codes_bytes;  // size of the code store (prefetch bound)
     int nqs;               // query states in flight (ws_nqs(K)), from the host
     int wsz;               // per-warp candidate buffer / sort scratch keys (ws_wsz(K)), from the host
@@ -507,11 +514,33 @@ struct WsBuild {
         uint8_t* lb = lut + ((size_t)jr * N + 4 * u) * E;
         // two owned rows per iteration: 2 x ng independent entry chains in flight
         int i = 0;
+        // Codebook in global memory (L2-resident), WS_GMEM_PF: the next
+        // iteration's two rows are loaded while this one computes (4 rows in
+        // flight per thread).  cfg3 p8: 53% of the builders' stall samples are
+        // long-scoreboard waits on these loads, but the builders also wait 30%
+        // of the time for free slots on layout A, and the prefetch's spills
+        // cost more than it saves there (78.8 -> 80.5 ms); off by default.
+        uint32_t pf0[CPI], pf1[CPI];
+        if constexpr (GMEM && WS_GMEM_PF) {
+            row(i0, pf0);
+            row(i0 + 1, pf1);
+        }
 #pragma unroll 1
         for (; i + 2 <= jpt; i += 2) {
             uint32_t c0[CPI], c1[CPI];
-            row(i0 + i, c0);
-            row(i0 + i + 1, c1);
+            if constexpr (GMEM && WS_GMEM_PF) {
+#pragma unroll
+                for (int k = 0; k < CPI; ++k) {
+                    c0[k] = pf0[k];
+                    c1[k] = pf1[k];
+                }
+                // rows past the chunk / the thread's share read valid rows or zeros
+                row(i0 + i + 2, pf0);
+                row(i0 + i + 3, pf1);
+            } else {
+                row(i0 + i, c0);
+                row(i0 + i + 1, c1);
+            }
             if constexpr (!GMEM) tmem_wait_ld();
             u64 cenA[2][SUB_D], cenB[2][SUB_D];
 #pragma unroll
@@ -879,7 +908,7 @@ __device__ __forceinline__ bool ws_grab(WsJobTab& T, int* cnt, int slot, uint32_
         k = __shfl_sync(0xffffffffu, k, 0);
     }
     if (2 * k >= T.nblk) return false;
-    if (C::SCAN_PF && !CH && pf_end != nullptr) {
+    if (!CH && pf_end != nullptr) {
         // bulk L2 prefetch of the two blocks WS_PF_PAIRS rounds of pairs ahead
         const int bf = 2 * (k + WS_PF_PAIRS * C::SW);
         if (bf < T.nblk) {
@@ -1033,7 +1062,7 @@ __device__ void ws_scanner(const ScanArgs& a, const WsArgs& w, WsJob* jobs, int*
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
     const uint8_t* codes = a.codes;
     // end of the code store when the scanners bulk-prefetch into L2 (else null)
-    const uint8_t* pf_end = w.l2pf ? codes + (size_t)w.n_codes_bytes : nullptr;
+    const uint8_t* pf_end = (w.l2pf & 2) ? codes + (size_t)w.n_codes_bytes : nullptr;
     uint4 A[NS], B[NS];
     uint32_t idA = 0, idB = 0;
     int slot = 0, ph = 0;
@@ -1227,6 +1256,53 @@ __global__ void __launch_bounds__(256) ws_plan_kernel(const ScanArgs a, int G, i
         pend += __popc(m);
         __syncwarp();
         const bool more = base + 32 < a.P;
+        if (!more && base == 0 && WS_PLAN_BALANCE) {
+            // All of the query's lists are known (P <= 32): group them into
+            // nJ = ceil(n / G) jobs of balanced total length instead of probe
+            // order -- rank by length, deal the ranks out in snake order
+            // (round r: jobs 0..nJ-1, then nJ-1..0).  A job's scan time is
+            // proportional to its vectors while its LUT build time is fixed,
+            // so uneven jobs leave the builders waiting for free slots on long
+            // jobs and the scanners waiting for LUTs on short ones (cfg2:
+            // coefficient of variation of a job's length 0.33 -> 0.09).  The
+            // result does not depend on the grouping: the top-k keys
+            // (R, id) are a total order.  Measured slower at cfg2 / cfg4 e5m3
+            // (3.74 -> 3.80 ms, 8.56 -> 8.88 ms): probe order scans the nearest
+            // lists first, which tightens the top-k threshold early (fewer
+            // offers); so it is off by default (WS_PLAN_BALANCE).
+            const int n = pend;  // <= 32, one entry per lane
+            int my_len = lane < n ? lenq[lane] : -1;
+            int my_lc = lane < n ? lcq[lane] : 0;
+            long long my_off = lane < n ? offq[lane] : 0;
+            int rank = 0;
+            for (int i = 0; i < n; ++i) {
+                const int li = __shfl_sync(0xffffffffu, my_len, i);
+                rank += (li > my_len || (li == my_len && i < lane)) ? 1 : 0;
+            }
+            const int nJ = (n + G - 1) / G;
+            const int full = n / nJ, rem = n % nJ;  // full rounds, entries of the partial round
+            const int rd = rank / nJ, pos = rank % nJ;
+            const int job = (rd & 1) ? nJ - 1 - pos : pos;
+            // job j holds `full` entries, one more if the partial round reached it
+            auto partial_before = [&](int j) {  // jobs < j that the partial round reached
+                return (full & 1) ? max(0, j - (nJ - rem)) : min(j, rem);
+            };
+            const int dst = job * full + partial_before(job) + rd;
+            __syncwarp();
+            if (lane < n) {
+                lcq[dst] = my_lc;
+                lenq[dst] = my_len;
+                offq[dst] = my_off;
+            }
+            __syncwarp();
+            for (int j = 0; j < nJ; ++j) {
+                const int from = j * full + partial_before(j);
+                const int cnt = full + (partial_before(j + 1) - partial_before(j));
+                emit(from, cnt, j == nJ - 1);
+            }
+            pend = 0;
+            break;
+        }
         int taken = 0;
         // emit full jobs; keep >= 1 pending until the end so the final job is marked last
         while (pend - taken > G || (!more && pend - taken > 0)) {
@@ -1411,7 +1487,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) scan_ws_kernel(const WsArgs w) 
             // jobs ahead overflowed L2 at cfg5: 225 GB of DRAM reads for 113 GB
             // of codes.)  With an L2-resident store it only adds requests (cfg2
             // +1.7%), so it is off there.
-            if (w.l2pf && PJ->h == 0 && t < PJ->ng) {
+            if ((w.l2pf & 1) && PJ->h == 0 && t < PJ->ng) {
                 // only the job's first 2 * WS_PF_PAIRS(SW) blocks: the scanners
                 // prefetch the rest a fixed distance ahead of their grabs
                 const int win = 2 * WS_PF_PAIRS * C::SW;
