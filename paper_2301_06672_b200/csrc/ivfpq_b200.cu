@@ -671,25 +671,15 @@ int run_scan_ws(ivfpq_index* idx, ScanArgs a, int64_t nq, int64_t P, int64_t K, 
     w.NBUF = plan.NBUF;
     w.gmem = plan.gmem;
     // code store larger than L2: builders prefetch each job's start; the
-    // scanners prefetch ahead of their grabs in layout B (IVFPQ_WS_SPF=0/1
-    // overrides the scanner part, for measurements)
+    // scanners prefetch ahead of their grabs in layout B (IVFPQ_WS_SPF=0
+    // turns the scanner part off, for measurements; the layout-A kernels are
+    // built without it: measured no gain at cfg3 p8 / cfg4)
     static const int env_spf = [] {
         const char* e = getenv("IVFPQ_WS_SPF");
         return e ? atoi(e) : -1;
     }();
     const bool spf = env_spf >= 0 ? env_spf != 0 : C::SCAN_PF;
     w.l2pf = (int64_t)idx->n_local * idx->s_pad > idx->l2_bytes ? (1 | (spf ? 2 : 0)) : 0;
-    // prefetch distance and the code loads' L2 policy (IVFPQ_WS_PFD / IVFPQ_WS_POL: measurements only)
-    static const int env_pfd = [] {
-        const char* e = getenv("IVFPQ_WS_PFD");
-        return e ? atoi(e) : 0;
-    }();
-    static const int env_pol = [] {
-        const char* e = getenv("IVFPQ_WS_POL");
-        return e ? atoi(e) : -1;
-    }();
-    w.pf_pairs = env_pfd > 0 ? env_pfd : WS_PF_PAIRS;
-    w.pol = env_pol >= 0 && env_pol <= 2 ? env_pol : 0;
     w.n_codes_bytes = (long long)idx->n_local * idx->s_pad;
     w.nqs = ws_nqs((int)K);
     w.wsz = ws_wsz((int)K);

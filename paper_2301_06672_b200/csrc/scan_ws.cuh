@@ -102,7 +102,7 @@ constexpr int WS_PRIV_K = 128;               // K up to which every scanner warp
 #ifndef WS_GMEM_PF
 #define WS_GMEM_PF 0                         // builders load global-memory codebook rows one iteration ahead (measured: no gain on layout A)
 #endif
-constexpr int WS_PF_PAIRS = 2;               // default L2 prefetch distance, in rounds of pairs (x SW pairs)
+constexpr int WS_PF_PAIRS = 2;               // L2 prefetch distance, in rounds of pairs (x SW pairs)
 // per-warp candidate buffer + sort scratch, each: WBUF keys, or K in the
 // private mode (a merged list is written there)
 __host__ __device__ constexpr int ws_wsz(int K) { return K <= WS_PRIV_K && K > WS_WBUF ? K : WS_WBUF; }
@@ -125,9 +125,7 @@ struct WsArgs {
     int NBUF;
     int gmem;              // 1: builders read the codebook from global memory (does not fit TMEM)
     int l2pf;              // code store > L2: bit 0 builders bulk-prefetch each job's start into L2,
-                           // bit 1 scanners prefetch pf_pairs rounds of pairs ahead of their grabs
-    int pf_pairs;          // L2 prefetch distance in rounds of pairs (WS_PF_PAIRS unless overridden)
-    int pol;               // L2 policy of the scanners' code loads: 0 evict_last, 1 evict_normal, 2 evict_first
+                           // bit 1 scanners prefetch WS_PF_PAIRS rounds of pairs ahead of their grabs
     long long n_codes_bytes;  // size of the code store (prefetch bound)
     int nqs;               // query states in flight (ws_nqs(K)), from the host
     int wsz;               // per-warp candidate buffer / sort scratch keys (ws_wsz(K)), from the host
@@ -900,7 +898,7 @@ struct WsJobTab {
 template <class C, bool CH>
 __device__ __forceinline__ bool ws_grab(WsJobTab& T, int* cnt, int slot, uint32_t slot_base, uint32_t lut_each,
                                         const uint8_t* codes, int s_pad, int rcc, int lane, WsPair& p,
-                                        const uint8_t* pf_end, int pfd) {
+                                        const uint8_t* pf_end) {
     int k = 0;
     if constexpr (CH) {
         k = T.next;
@@ -910,9 +908,9 @@ __device__ __forceinline__ bool ws_grab(WsJobTab& T, int* cnt, int slot, uint32_
         k = __shfl_sync(0xffffffffu, k, 0);
     }
     if (2 * k >= T.nblk) return false;
-    if (!CH && pf_end != nullptr) {
-        // bulk L2 prefetch of the two blocks pfd rounds of pairs ahead
-        const int bf = 2 * (k + pfd * C::SW);
+    if (C::SCAN_PF && !CH && pf_end != nullptr) {
+        // bulk L2 prefetch of the two blocks WS_PF_PAIRS rounds of pairs ahead
+        const int bf = 2 * (k + WS_PF_PAIRS * C::SW);
         if (bf < T.nblk) {
             int gf, nbf, vof;
             T.block(bf, gf, nbf, vof);
@@ -1061,13 +1059,12 @@ __device__ void ws_scanner(const ScanArgs& a, const WsArgs& w, WsJob* jobs, int*
     u64* part = CH ? reinterpret_cast<u64*>(w.part) + ((size_t)blockIdx.x * C::SW + sw) * w.maxp * 32 + lane : nullptr;
     const int s_pad = a.s_pad;
     u64 pol;
-    if (w.pol == 2) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    else if (w.pol == 1) asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
-    else asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    const int pfd = w.pf_pairs;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
     const uint8_t* codes = a.codes;
     // end of the code store when the scanners bulk-prefetch into L2 (else null)
-    const uint8_t* pf_end = (w.l2pf & 2) ? codes + (size_t)w.n_codes_bytes : nullptr;
+    // (compiled in for the layouts that use it only: its pointer costs
+    // registers, and the layout-A kernels spill without it otherwise)
+    const uint8_t* pf_end = C::SCAN_PF && (w.l2pf & 2) ? codes + (size_t)w.n_codes_bytes : nullptr;
     uint4 A[NS], B[NS];
     uint32_t idA = 0, idB = 0;
     int slot = 0, ph = 0;
@@ -1076,7 +1073,7 @@ __device__ void ws_scanner(const ScanArgs& a, const WsArgs& w, WsJob* jobs, int*
     mbar_wait(full, 0);
     if (jobs[0].qs < 0) return;
     ct.load(jobs, lane, sw);
-    bool have = ws_grab<C, CH>(ct, cnt, 0, lut_s0, lut_each, codes, s_pad, rcc, lane, cur, pf_end, pfd);
+    bool have = ws_grab<C, CH>(ct, cnt, 0, lut_s0, lut_each, codes, s_pad, rcc, lane, cur, pf_end);
     auto load_first = [&](const WsPair& p) {
 #pragma unroll
         for (int u = 0; u < NS; ++u)
@@ -1099,13 +1096,13 @@ __device__ void ws_scanner(const ScanArgs& a, const WsArgs& w, WsJob* jobs, int*
             if (jobs[slot].qs < 0) break;
             ct.load(jobs + slot, lane, sw);
             have = ws_grab<C, CH>(ct, cnt, slot, lut_s0 + (uint32_t)slot * slot_bytes, lut_each, codes, s_pad, rcc, lane,
-                               cur, pf_end, pfd);
+                               cur, pf_end);
             if (have) load_first(cur);
             continue;
         }
         // ---- the next pair: same job, else the next job if its LUTs are ready
         bool hn = ws_grab<C, CH>(ct, cnt, slot, lut_s0 + (uint32_t)slot * slot_bytes, lut_each, codes, s_pad, rcc, lane,
-                              nxt, pf_end, pfd);
+                              nxt, pf_end);
         bool cross = false;
         if (!hn) {
             const int ns = slot + 1 == NBUF ? 0 : slot + 1;
@@ -1115,7 +1112,7 @@ __device__ void ws_scanner(const ScanArgs& a, const WsArgs& w, WsJob* jobs, int*
             if (NBUF > 1 && mbar_test(full + ns, (uint32_t)nph) && jobs[ns].qs >= 0) {
                 nt.load(jobs + ns, lane, sw);
                 hn = ws_grab<C, CH>(nt, cnt, ns, lut_s0 + (uint32_t)ns * slot_bytes, lut_each, codes, s_pad, rcc, lane,
-                                 nxt, pf_end, pfd);
+                                 nxt, pf_end);
                 cross = true;  // (an empty next job is left to the blocking path)
             }
         }
@@ -1487,15 +1484,15 @@ __global__ void __launch_bounds__(C::THREADS, 1) scan_ws_kernel(const WsArgs w) 
             // register prefetch of one pair ahead does not cover the DRAM
             // latency, so codes are also pulled into L2 with bulk prefetches: the
             // start of the job here (a list's codes are one contiguous range in
-            // the interleaved layout), the rest by the scanners, pf_pairs
+            // the interleaved layout), the rest by the scanners, WS_PF_PAIRS
             // rounds of pairs ahead of their grabs.  (Whole jobs prefetched NBUF
             // jobs ahead overflowed L2 at cfg5: 225 GB of DRAM reads for 113 GB
             // of codes.)  With an L2-resident store it only adds requests (cfg2
             // +1.7%), so it is off there.
             if ((w.l2pf & 1) && PJ->h == 0 && t < PJ->ng) {
-                // only the job's first 2 * pf_pairs * SW blocks: the scanners
+                // only the job's first 2 * WS_PF_PAIRS(SW) blocks: the scanners
                 // prefetch the rest a fixed distance ahead of their grabs
-                const int win = 2 * w.pf_pairs * C::SW;
+                const int win = 2 * WS_PF_PAIRS * C::SW;
                 const int b0 = PJ->pref[t], b1 = min(PJ->pref[t + 1], win);
                 if (b0 < b1) {
                     const int nv = min(PJ->len[t], (b1 - b0) * 32);
