@@ -21,6 +21,27 @@ namespace ivfpq {
 
 constexpr int CL_BQ = 64, CL_BC = 64, CL_BK = 16;
 
+// packed f32x2 sub / mul: two IEEE ops with one rounding each, as the scalar
+// __fsub_rn / __fmul_rn; the adds stay scalar so nothing can be contracted
+__device__ __forceinline__ unsigned long long cl_pk2(float a, float b) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void cl_upk2(unsigned long long v, float& a, float& b) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ unsigned long long cl_sub2(unsigned long long a, unsigned long long b) {
+    unsigned long long r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ unsigned long long cl_mul2(unsigned long long a, unsigned long long b) {
+    unsigned long long r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+
 __global__ void __launch_bounds__(256)
 coarse_l2_kernel(const float* __restrict__ Q, int nq, const float* __restrict__ C, int nc, int d,
                  float* __restrict__ D) {
@@ -47,14 +68,21 @@ coarse_l2_kernel(const float* __restrict__ Q, int nq, const float* __restrict__ 
         for (int kk = 0; kk < CL_BK; ++kk) {
             float4 qv = *reinterpret_cast<const float4*>(&Qs[kk][ty * 4]);
             float4 cv = *reinterpret_cast<const float4*>(&Cs[kk][tx * 4]);
-            float qa[4] = {qv.x, qv.y, qv.z, qv.w}, ca[4] = {cv.x, cv.y, cv.z, cv.w};
+            const float qa[4] = {qv.x, qv.y, qv.z, qv.w};
+            // 2 instructions per element (packed sub + mul, scalar add) instead of 3
+            const unsigned long long c01 = cl_pk2(cv.x, cv.y), c23 = cl_pk2(cv.z, cv.w);
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    float df = __fsub_rn(ca[j], qa[i]);
-                    acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(df, df));
-                }
+            for (int i = 0; i < 4; ++i) {
+                const unsigned long long qq = cl_pk2(qa[i], qa[i]);
+                const unsigned long long d01 = cl_sub2(c01, qq), d23 = cl_sub2(c23, qq);
+                float s0, s1, s2, s3;
+                cl_upk2(cl_mul2(d01, d01), s0, s1);
+                cl_upk2(cl_mul2(d23, d23), s2, s3);
+                acc[i][0] = __fadd_rn(acc[i][0], s0);
+                acc[i][1] = __fadd_rn(acc[i][1], s1);
+                acc[i][2] = __fadd_rn(acc[i][2], s2);
+                acc[i][3] = __fadd_rn(acc[i][3], s3);
+            }
         }
         __syncthreads();
     }
