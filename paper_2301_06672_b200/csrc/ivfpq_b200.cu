@@ -125,6 +125,8 @@ struct ivfpq_index {
     DevBuf q, dist, pkeys, oids, odist, oshort, keys, ncand, work, plan_jobs, plan_rq, plan_nj, plan_nc, tc_sl, flags, glut,
         part;
     int64_t max_len = 0;  // longest owned list (chunked scan: partial-sum scratch per warp)
+    int32_t* h_short = nullptr;  // pinned host copy of the short flags (ivfpq_search)
+    int64_t h_short_cap = 0;
     int num_sms = 0;
     int64_t l2_bytes = 0;  // device L2 size (scan: bulk L2 prefetch when the code store exceeds it)
 };
@@ -1027,6 +1029,7 @@ int ivfpq_index_destroy(ivfpq_index* idx) {
         b->release();
     if (idx->stream) cudaStreamDestroy(idx->stream);
     if (idx->last_ev) cudaEventDestroy(idx->last_ev);
+    if (idx->h_short) cudaFreeHost(idx->h_short);
     delete idx;
     return IVFPQ_OK;
 }
@@ -1056,11 +1059,20 @@ int ivfpq_search(ivfpq_index* idx, const float* queries, int64_t nq, int64_t k, 
         CK(cudaMemcpyAsync(out_ids, idx->oids.p, (size_t)nq * k * 8, cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(out_dists, idx->odist.p, (size_t)nq * k * 4, cudaMemcpyDeviceToHost, st));
     }
-    std::vector<int32_t> sh((size_t)nq);
-    if (nq > 0) CK(cudaMemcpyAsync(sh.data(), idx->oshort.p, (size_t)nq * 4, cudaMemcpyDeviceToHost, st));
+    // short flags into a pinned per-handle buffer (an async copy; a pageable
+    // destination would be staged synchronously)
+    if (nq > idx->h_short_cap) {
+        CK(cudaStreamSynchronize(st));
+        if (idx->h_short) CK(cudaFreeHost(idx->h_short));
+        idx->h_short = nullptr;
+        idx->h_short_cap = 0;
+        CK(cudaHostAlloc((void**)&idx->h_short, (size_t)nq * 4, cudaHostAllocDefault));
+        idx->h_short_cap = nq;
+    }
+    if (nq > 0) CK(cudaMemcpyAsync(idx->h_short, idx->oshort.p, (size_t)nq * 4, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     int64_t ns = 0;
-    for (int32_t v : sh) ns += v;
+    for (int64_t i = 0; i < nq; ++i) ns += idx->h_short[i];
     if (out_n_short) *out_n_short = ns;
     return IVFPQ_OK;
 }
